@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""Benchmark: AnyBCQ bit-plane GEMV on B200 (BASELINE.json configs[1]).
+
+One *step* = the Llama-3-8B layer-shape sweep (q, k, v, o, gate, up, down)
+GEMV at batch 1 for every precision p in {2, 3, 4} (21 GEMVs), on synthetic
+packed planes (splitmix64 words) and fp16 scales, x in fp16, y in fp16.
+
+  value  = algorithmic bytes of the step / device time  [GB/s]
+           (bytes = p-plane bytes + scale-set-p bytes + x + y)
+  e2e    = the same through the public API with pinned HOST x/y
+           (H2D of x + D2H of y per GEMV inside the timed region)
+  roofline: the LUT kernel is the only kernel in the step; achieved =
+           algorithmic bytes / kernel time, peak = MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline: the reference's LUT algorithm restated in C (oracle/),
+           all host threads, on a bounded sample of the same workload
+
+L2: three copies of the layer set (one per precision) so that every plane
+byte is re-read only after a full step (>= 245 MB > 126 MB L2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+For N > 1 (torchrun): each rank holds a 1/N row shard of layers N x taller
+(per-rank work = the 1-GPU step, weak scaling) and every GEMV output is
+all-gathered over NCCL.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+          ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+PRECISIONS = (2, 3, 4)
+P_LO, P_HI = 2, 4
+SCALE_BYTES = 2   # fp16 scales
+XY_BYTES = 2      # fp16 x and y
+METRIC = "bit-plane GEMV HBM GB/s (Llama-3-8B layer sweep, p=2/3/4, batch 1)"
+
+
+def algo_bytes(rows: int, cols: int, p: int) -> int:
+    """p*N*K/8 + p*N*(K/128)*s_w + K*2 + N*2 (symmetric)."""
+    G = -(-cols // 128)
+    return p * rows * cols // 8 + p * rows * G * SCALE_BYTES + cols * XY_BYTES + rows * XY_BYTES
+
+
+def step_bytes() -> int:
+    return sum(algo_bytes(r, c, p) for p in PRECISIONS for _, r, c in LAYERS)
+
+
+# ---------------------------------------------------------------------------
+def read_peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx, self.rows, self.proc = gpu_index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def make_layer_models(P, row_scale: int, copies: int, seed0: int = 0):
+    """copies x 7 DeviceModels (p 2:4, fp16 scales), synthetic planes/scales
+    generated on the host from splitmix64."""
+    from oracle import anybcq_oracle as O  # synthetic-input generator only (not measured)
+
+    models = []
+    for c in range(copies):
+        row = []
+        for li, (name, r, k) in enumerate(LAYERS):
+            rows = r * row_scale
+            seed = seed0 + 1000 * c + li
+            dm = P.DeviceModel(rows, k, 128, P_LO, P_HI, False, scale_dtype="f16")
+            dm.load_planes(O.random_words(P_HI, rows, k, seed=seed))
+            rng = np.random.default_rng(seed)
+            for p in PRECISIONS:
+                a = (0.01 + 0.1 * np.abs(rng.standard_normal((p, rows, k // 128)))).astype(np.float32)
+                dm.load_scale_set(p, a)
+            row.append(dm)
+        models.append(row)
+    return models
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_10467_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    copies = len(PRECISIONS)
+    models = make_layer_models(P, 1, copies, seed0=17 * rank)
+    xs = {k: (torch.randn(k, device=dev) * 1.0).half() for k in {c for _, _, c in LAYERS}}
+    ys = [[torch.empty(m.rows, dtype=torch.float16, device=dev) for m in row] for row in models]
+    gathered = None
+    if world > 1:
+        gathered = [[torch.empty(m.rows * world, dtype=torch.float16, device=dev) for m in row] for row in models]
+
+    stream = torch.cuda.Stream(device=dev)
+
+    def step_launches():
+        for pi, p in enumerate(PRECISIONS):
+            for li, m in enumerate(models[pi]):
+                m.gemv(p, xs[m.cols], out=ys[pi][li], stream=stream)
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
+
+    # warm up (allocates per-stream workspaces), then capture one step as a graph
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step_launches()
+    torch.cuda.synchronize()
+    use_graph = world == 1
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step_launches()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, events on the launching stream ------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                if use_graph:
+                    graph.replay()
+                else:
+                    step_launches()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.05)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    total_bytes = step_bytes() * world
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # ---- per-shape breakdown (device time, back-to-back launches) ----------
+    per_shape = {}
+    if rank == 0:
+        reps = 20
+        for li, (name, r, k) in enumerate(LAYERS):
+            for pi, p in enumerate(PRECISIONS):
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2, stream=stream):
+                    for j in range(reps):
+                        models[j % copies][li].gemv(p, xs[k], out=ys[j % copies][li], stream=stream)
+                g2.replay()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(5):
+                    g2.replay()
+                b.record(stream)
+                torch.cuda.synchronize()
+                us = a.elapsed_time(b) * 1e3 / (5 * reps)
+                per_shape[f"{name}_{r}x{k}_p{p}"] = {
+                    "us": round(us, 3), "GBps": round(algo_bytes(r, k, p) / (us * 1e-6) / 1e9, 1)}
+
+        # cuBLAS fp16 GEMV comparator (dense fp16 weights, one copy > L2)
+        dense = [torch.randn(r, k, device=dev, dtype=torch.float16) * 0.01 for _, r, k in LAYERS]
+        yd = [torch.empty(r, device=dev, dtype=torch.float16) for _, r, _ in LAYERS]
+        gd = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gd, stream=stream):
+            for li, (_, r, k) in enumerate(LAYERS):
+                torch.mv(dense[li], xs[k], out=yd[li])
+        gd.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(20):
+            gd.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        fp16_us = a.elapsed_time(b) * 1e3 / 20
+        fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)
+        p2_us = sum(per_shape[f"{n}_{r}x{k}_p2"]["us"] for n, r, k in LAYERS)
+        fp16 = {"us_per_sweep": round(fp16_us, 2), "GBps": round(fp16_bytes / (fp16_us * 1e-6) / 1e9, 1),
+                "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2)}
+        del dense
+
+    # ---- e2e: public API with pinned host buffers, copies in the timed region
+    e2e = None
+    if rank == 0:
+        hx = {k: xs[k].cpu().pin_memory() for k in xs}
+        hy = [[torch.empty(m.rows, dtype=torch.float16).pin_memory() for m in row] for row in models]
+        dx = {k: torch.empty_like(xs[k]) for k in xs}
+        h2d = d2h = 0
+
+        def e2e_step():
+            nonlocal h2d, d2h
+            for pi, p in enumerate(PRECISIONS):
+                for li, m in enumerate(models[pi]):
+                    dx[m.cols].copy_(hx[m.cols], non_blocking=True)
+                    y = m.gemv(p, dx[m.cols], out=ys[pi][li], stream=stream)
+                    hy[pi][li].copy_(y, non_blocking=True)
+                    h2d += hx[m.cols].numel() * 2
+                    d2h += y.numel() * 2
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                e2e_step()
+            torch.cuda.synchronize()
+            h2d = d2h = 0
+            n_e2e = max(3, min(args.steps, 20))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(n_e2e):
+                e2e_step()
+            b.record(stream)
+            torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / n_e2e
+        e2e = {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d // n_e2e,
+               "d2h_bytes_per_step": d2h // n_e2e, "api": "DeviceModel.gemv (C ABI abcq_gemv) per call"}
+
+    if rank == 0:
+        peak, peak_kind = read_peaks()
+        kernel_bytes = step_bytes()
+        achieved = kernel_bytes / (ms_step * 1e-3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "ncu_traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text())
+            except Exception:
+                traffic = None
+        cpu = cpu_baseline() if world == 1 and not args.no_cpu else None
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
+            "config": {"workload": "Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, "
+                                   "p=2,3,4 per step, g=128, fp16 scales/x/y",
+                       "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
+                       "bytes_per_step": kernel_bytes,
+                       "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
+                             f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
+                       "timing": "CUDA graph of one step, CUDA events on the launch stream",
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
+            "gpu_launches": args.steps * len(LAYERS) * len(PRECISIONS),
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                         "kernel": "abcq::gemv_lut_kernel", "traffic": traffic,
+                         "algorithmic_bytes_per_step": kernel_bytes},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "per_shape": per_shape,
+            "fp16_cublas": fp16,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+def _cpu_sample_models():
+    from oracle import anybcq_oracle as O
+    out = []
+    for li, (name, r, k) in enumerate(LAYERS):
+        words = O.random_words(P_HI, r, k, seed=li)
+        rng = np.random.default_rng(li)
+        alphas = {p: (0.01 + 0.1 * np.abs(rng.standard_normal((p, r, k // 128)))).astype(np.float16)
+                  .astype(np.float32) for p in PRECISIONS}
+        out.append((name, r, k, words, alphas))
+    return out
+
+
+def cpu_baseline(repeats: int = 2):
+    """The reference LUT algorithm (C port of gemv.py:67-95,188-222) on all host
+    cores, over the full layer sweep (the GPU step's workload), `repeats` times."""
+    from oracle import c_oracle
+
+    threads = c_oracle.cpu_threads()
+    models = _cpu_sample_models()
+    x = {k: np.random.default_rng(k).standard_normal(k).astype(np.float16).astype(np.float64)
+         for k in {c for _, _, c in LAYERS}}
+    for name, r, k, words, alphas in models[:1]:
+        c_oracle.lut_gemv(words, k, 128, alphas[2], None, 2, x[k], threads)  # warm
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        for p in PRECISIONS:
+            for name, r, k, words, alphas in models:
+                c_oracle.lut_gemv(words, k, 128, alphas[p], None, p, x[k], threads)
+    dt = (time.perf_counter() - t0) / repeats
+    return {"value": round(step_bytes() / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "ms_per_step": round(dt * 1e3, 1),
+            "sample": f"full layer sweep (21 GEMVs) x{repeats}, C restatement of GemvEngine.lut, "
+                      f"{threads} pthreads"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (C port) on this workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import c_oracle
+
+    threads = c_oracle.cpu_threads()
+    models = _cpu_sample_models()
+    x = {k: np.random.default_rng(k).standard_normal(k).astype(np.float16).astype(np.float64)
+         for k in {c for _, _, c in LAYERS}}
+
+    def one_step():
+        for p in PRECISIONS:
+            for name, r, k, words, alphas in models:
+                c_oracle.lut_gemv(words, k, 128, alphas[p], None, p, x[k], threads)
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = round(step_bytes() / dt / 1e9, 3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": {"workload": "Llama-3-8B layer sweep GEMV, batch 1, p=2,3,4"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": "full layer sweep per step (C restatement of GemvEngine.lut; "
+                                   "reference is Python+numba, no compiled sources to build)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * anybcq_b200.h -- C ABI of the B200-native AnyBCQ bit-plane matmul.
+ *
+ * Drop-in boundary for the reference's GEMV engine. The reference
+ * (/root/reference/pkg/src/anybcq) is pure Python + one numba kernel and has
+ * no FFI of its own; its innermost compiled boundary is
+ *
+ *     _lut_kernel(idx, table, alpha, chunk_lo, chunk_hi, p_use,
+ *                 row_lo, row_hi, out)                    gemv.py:84-95
+ *
+ * driven by GemvEngine.lut / GemvEngine.naive (gemv.py:170-222) over a
+ * MultiPrecisionModel (progressive.py:32-79) whose planes use the packing of
+ * packing.py:1-37 and whose scale sets are bcq.ScaleTensor (bcq.py:50-96).
+ * Every entry point below states which reference interface it replaces.
+ *
+ * Conventions (all functions):
+ *   - plain pointers and sizes only; every `d_*` pointer is DEVICE memory
+ *     owned by the caller; `stream` is a cudaStream_t passed as void*
+ *     (NULL = legacy default stream); launches are asynchronous;
+ *   - return 0 on success, a NEGATIVE ABCQ_E* code for an invalid argument
+ *     (the Python layer raises anybcq's UsageError, gemv.py:148-156,
+ *     before any work is queued), a POSITIVE cudaError_t value for a CUDA
+ *     failure (Python raises RuntimeError);
+ *   - abcq_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef ANYBCQ_B200_H
+#define ANYBCQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ABCQ_ABI_VERSION 1
+#define ABCQ_MAX_PLANES 16 /* bcq.py:22 MAX_PLANES */
+
+/* element dtypes */
+#define ABCQ_F32 0
+#define ABCQ_F16 1
+
+/* plane layouts */
+#define ABCQ_LAYOUT_ROWMAJOR 0 /* reference layout verbatim: (p_hi, rows, ceil(cols/32)) u32 */
+#define ABCQ_LAYOUT_TILED 1    /* B200 tiled layout (group_size == 128) */
+
+/* argument errors (negative) */
+#define ABCQ_OK 0
+#define ABCQ_E_ARG -1       /* bad pointer / shape / dtype */
+#define ABCQ_E_PRECISION -2 /* p outside [p_lo, p_hi] (gemv.py:149-152) */
+#define ABCQ_E_LAYOUT -3    /* layout cannot serve this call */
+#define ABCQ_E_WORKSPACE -4 /* workspace too small */
+#define ABCQ_E_DEVICE -5    /* no sm_100 device / kernel image */
+
+/*
+ * A device-resident multi-precision model: ONE stack of p_hi planes shared by
+ * every precision plus an independent scale set (and offset set in
+ * asymmetric mode) per p in [p_lo, p_hi] -- progressive.py:32-79.
+ * alpha[p] / offset[p] are indexed by precision p (entries outside
+ * [p_lo, p_hi] are ignored). Layout of each buffer:
+ *   ROWMAJOR: planes (p_hi, rows, ceil(cols/32)) u32 as packing.py:1-7;
+ *             alpha[p] (p, rows, G) and offset[p] (rows, G), scale_dtype.
+ *   TILED:    as produced by abcq_pack_planes / abcq_pack_scales.
+ */
+typedef struct abcq_model {
+    int32_t rows;
+    int32_t cols;
+    int32_t group_size;
+    int32_t p_lo;
+    int32_t p_hi;
+    int32_t asymmetric;  /* 1: offsets present (bcq.py:31-47 mode) */
+    int32_t layout;      /* ABCQ_LAYOUT_* */
+    int32_t scale_dtype; /* ABCQ_F32 | ABCQ_F16 */
+    int64_t plane_stride_bytes; /* bytes between consecutive planes */
+    const void* planes;
+    const void* alpha[ABCQ_MAX_PLANES + 1];
+    const void* offset[ABCQ_MAX_PLANES + 1];
+} abcq_model_t;
+
+/* ---- library ------------------------------------------------------------ */
+int abcq_abi_version(void);
+const char* abcq_last_error(void);
+/* 0 if device `dev` is sm_100 and the sm_100a kernels load, else ABCQ_E_DEVICE */
+int abcq_device_check(int32_t dev);
+
+/* ---- layout sizes (host-only arithmetic) ---------------------------------
+ * Tiled layout: 16-row tiles x 256-column slices; see DESIGN.md §Layout.  */
+int abcq_tiled_plane_bytes(int32_t rows, int32_t cols, int64_t* out_bytes);
+int abcq_tiled_scale_elems(int32_t rows, int32_t cols, int32_t p,
+                           int64_t* out_alpha_elems, int64_t* out_offset_elems);
+
+/* ---- packing: replaces BitPlaneSet.words as the kernel's view ------------
+ * abcq_pack_planes: reference words (planes, rows, ceil(cols/32)) u32
+ * (packing.py:22-30, BitPlaneSet.words packing.py:40-52) -> tiled planes.
+ * A bijection on the code bits; abcq_unpack_planes is its inverse
+ * (padding bits come back zero, packing.py:6-7).                          */
+int abcq_pack_planes(const uint32_t* d_words, int32_t planes, int32_t rows, int32_t cols,
+                     void* d_tiled, void* stream);
+int abcq_unpack_planes(const void* d_tiled, int32_t planes, int32_t rows, int32_t cols,
+                       uint32_t* d_words, void* stream);
+/* ScaleTensor (bcq.py:50-96) of ONE precision p: alpha (p, rows, G) f32,
+ * offset (rows, G) f32 or NULL -> tiled scale set in `scale_dtype`
+ * (f16 = round-to-nearest-even, the container's scale_width=2 rounding,
+ * model_format.py:43-52). group_size must be 128.                          */
+int abcq_pack_scales(const float* d_alpha, const float* d_offset, int32_t p, int32_t rows,
+                     int32_t cols, int32_t group_size, int32_t scale_dtype,
+                     void* d_alpha_out, void* d_offset_out, void* stream);
+
+/* ---- lookup table: replaces LookupTable.build (gemv.py:67-81) -----------
+ * d_table (ceil(cols/mu), 2^mu) f32, bit-identical to the reference's
+ * doubling construction. Exposed for parity; the GEMV kernels build the
+ * same table in shared memory.                                            */
+int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk_width,
+                   float* d_table, void* stream);
+
+/* ---- GEMV: replaces GemvEngine.lut (gemv.py:188-222) ---------------------
+ * y = sum_{i<p} alpha^(p)_{i,g} (B_i x) [+ offset^(p) . groupsum(x)]
+ * for one request at precision p (runtime argument, no recompile).
+ * x: (cols) in x_dtype; y: (rows) in y_dtype. TILED layout -> the sm_100a
+ * LUT kernel; ROWMAJOR layout (any group size) -> the generic kernel.
+ * Workspace: >= abcq_gemv_workspace_bytes(); must be zero-filled once
+ * before first use and may not be shared by calls running concurrently
+ * (one workspace per stream).                                             */
+int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
+int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
+              int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ---- naive path: replaces GemvEngine.naive (gemv.py:170-186) ------------
+ * Column-by-column decode of the planes (either layout, any group size).   */
+int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype,
+                    void* d_y, int32_t y_dtype, void* stream);
+
+/* ---- dense reconstruction: replaces bcq.dequantize (bcq.py:372-378) -----
+ * d_w (rows, cols) in w_dtype = f32(sum_{i<p} alpha_i b_i [+ offset]) with
+ * the sum in f64 (bcq.py:137-152). Used for the dequant oracle and for the
+ * half-precision (cuBLAS) comparison weights.                              */
+int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANYBCQ_B200_H */

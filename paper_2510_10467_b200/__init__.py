@@ -1,0 +1,26 @@
+"""anybcq-b200: B200-native (sm_100a) AnyBCQ bit-plane matmul.
+
+Drop-in for the reference package's GEMV path (`anybcq.gemv`): the same
+entry points backed by hand-written CUDA in libanybcq_b200.so (C ABI:
+include/anybcq_b200.h). See DESIGN.md.
+"""
+
+from .errors import (AnyBcqError, BadMagicError, BadVersionError, ChecksumError, FileFormatError,
+                     NonFiniteError, TruncatedError, UnsupportedDtypeError, UsageError)
+from .model import (BitPlaneSet, MultiPrecisionModel, QuantConfig, ScaleTensor, group_bounds,
+                    group_count, pack_signs, precision_view, unpack_signs, words_per_row)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # torch-dependent modules load lazily so the host types import without CUDA
+    if name in ("GemvEngine", "GemvStats", "LookupTable", "BenchRow", "bench", "gemv_lut",
+                "gemv_naive", "dequant_oracle", "dense_gemv_reference", "render_bench_text",
+                "render_bench_csv"):
+        from . import engine
+        return getattr(engine, name)
+    if name == "DeviceModel":
+        from .device_model import DeviceModel
+        return DeviceModel
+    raise AttributeError(name)

@@ -1,0 +1,179 @@
+// abcq_capi.cu -- extern "C" entry points of libanybcq_b200.so (include/anybcq_b200.h).
+//
+// Argument checking happens here, before anything is queued, mirroring the
+// reference's validate-then-work order (gemv.py:148-156: UsageError for p
+// outside [p_lo, p_hi] or a wrong input length).
+#include <cstdarg>
+#include <cstdio>
+
+#include "abcq_common.cuh"
+#include "abcq_internal.h"
+
+namespace {
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_ret(int e, const char* what) {
+    if (e == 0) return 0;
+    return fail(e, "%s: CUDA error %d (%s)", what, e, cudaGetErrorString((cudaError_t)e));
+}
+
+bool dtype_ok(int d) { return d == ABCQ_F32 || d == ABCQ_F16; }
+
+int check_model(const abcq_model_t* m) {
+    if (!m) return fail(ABCQ_E_ARG, "model is NULL");
+    if (m->rows < 1 || m->cols < 1) return fail(ABCQ_E_ARG, "bad shape %dx%d", m->rows, m->cols);
+    if (m->group_size < 1) return fail(ABCQ_E_ARG, "group_size must be >= 1");
+    if (!(1 <= m->p_lo && m->p_lo <= m->p_hi && m->p_hi <= ABCQ_MAX_PLANES))
+        return fail(ABCQ_E_ARG, "invalid precision range [%d, %d]", m->p_lo, m->p_hi);
+    if (!dtype_ok(m->scale_dtype)) return fail(ABCQ_E_ARG, "bad scale dtype %d", m->scale_dtype);
+    if (m->layout != ABCQ_LAYOUT_ROWMAJOR && m->layout != ABCQ_LAYOUT_TILED)
+        return fail(ABCQ_E_ARG, "bad layout %d", m->layout);
+    if (m->layout == ABCQ_LAYOUT_TILED && m->group_size != abcq::kGroup)
+        return fail(ABCQ_E_LAYOUT, "tiled layout requires group_size 128, got %d", m->group_size);
+    if (!m->planes) return fail(ABCQ_E_ARG, "planes pointer is NULL");
+    return 0;
+}
+
+int check_call(const abcq_model_t* m, int p, const void* x, int xd, const void* y, int yd) {
+    if (int rc = check_model(m)) return rc;
+    if (p < m->p_lo || p > m->p_hi)
+        return fail(ABCQ_E_PRECISION, "precision %d outside [%d, %d]", p, m->p_lo, m->p_hi);
+    if (!m->alpha[p]) return fail(ABCQ_E_ARG, "scale set %d missing", p);
+    if (m->asymmetric && !m->offset[p]) return fail(ABCQ_E_ARG, "offset set %d missing", p);
+    if (!x || !y) return fail(ABCQ_E_ARG, "x / y pointer is NULL");
+    if (!dtype_ok(xd) || !dtype_ok(yd)) return fail(ABCQ_E_ARG, "bad x/y dtype");
+    return 0;
+}
+}  // namespace
+
+namespace abcq {
+int num_sms() {
+    static int cached = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cached < 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cached = v;
+    }
+    return cached;
+}
+}  // namespace abcq
+
+extern "C" {
+
+int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
+
+const char* abcq_last_error(void) { return g_err; }
+
+int abcq_device_check(int32_t dev) {
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return fail(ABCQ_E_DEVICE, "no CUDA device %d: %s", dev, cudaGetErrorString(e));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(ABCQ_E_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a only",
+                    dev, prop.major, prop.minor);
+    e = (cudaError_t)abcq::probe_kernel_image();
+    if (e != cudaSuccess) return fail(ABCQ_E_DEVICE, "sm_100a kernel image unusable: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+int abcq_tiled_plane_bytes(int32_t rows, int32_t cols, int64_t* out_bytes) {
+    if (rows < 1 || cols < 1 || !out_bytes) return fail(ABCQ_E_ARG, "bad arguments");
+    *out_bytes = abcq::tiled_plane_bytes(rows, cols);
+    return 0;
+}
+
+int abcq_tiled_scale_elems(int32_t rows, int32_t cols, int32_t p, int64_t* out_alpha, int64_t* out_offset) {
+    if (rows < 1 || cols < 1 || p < 1 || p > ABCQ_MAX_PLANES || !out_alpha || !out_offset)
+        return fail(ABCQ_E_ARG, "bad arguments");
+    *out_alpha = abcq::tiled_alpha_elems(rows, cols, p);
+    *out_offset = abcq::tiled_offset_elems(rows, cols);
+    return 0;
+}
+
+int abcq_pack_planes(const uint32_t* d_words, int32_t planes, int32_t rows, int32_t cols, void* d_tiled,
+                     void* stream) {
+    if (!d_words || !d_tiled || planes < 1 || planes > ABCQ_MAX_PLANES || rows < 1 || cols < 1)
+        return fail(ABCQ_E_ARG, "abcq_pack_planes: bad arguments");
+    return cuda_ret(abcq::launch_pack_planes(d_words, planes, rows, cols, d_tiled, (cudaStream_t)stream),
+                    "abcq_pack_planes");
+}
+
+int abcq_unpack_planes(const void* d_tiled, int32_t planes, int32_t rows, int32_t cols, uint32_t* d_words,
+                       void* stream) {
+    if (!d_words || !d_tiled || planes < 1 || planes > ABCQ_MAX_PLANES || rows < 1 || cols < 1)
+        return fail(ABCQ_E_ARG, "abcq_unpack_planes: bad arguments");
+    return cuda_ret(abcq::launch_unpack_planes(d_tiled, planes, rows, cols, d_words, (cudaStream_t)stream),
+                    "abcq_unpack_planes");
+}
+
+int abcq_pack_scales(const float* d_alpha, const float* d_offset, int32_t p, int32_t rows, int32_t cols,
+                     int32_t group_size, int32_t scale_dtype, void* d_alpha_out, void* d_offset_out,
+                     void* stream) {
+    if (!d_alpha || !d_alpha_out || p < 1 || p > ABCQ_MAX_PLANES || rows < 1 || cols < 1)
+        return fail(ABCQ_E_ARG, "abcq_pack_scales: bad arguments");
+    if (group_size != abcq::kGroup)
+        return fail(ABCQ_E_LAYOUT, "abcq_pack_scales: tiled scales need group_size 128, got %d", group_size);
+    if (!dtype_ok(scale_dtype)) return fail(ABCQ_E_ARG, "abcq_pack_scales: bad dtype");
+    if (d_offset && !d_offset_out) return fail(ABCQ_E_ARG, "abcq_pack_scales: offset output missing");
+    return cuda_ret(abcq::launch_pack_scales(d_alpha, d_offset, p, rows, cols, scale_dtype, d_alpha_out,
+                                             d_offset_out, (cudaStream_t)stream),
+                    "abcq_pack_scales");
+}
+
+int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk_width, float* d_table,
+                   void* stream) {
+    if (chunk_width < 1 || chunk_width > 8)
+        return fail(ABCQ_E_ARG, "chunk width must be in [1, 8], got %d", chunk_width);
+    if (!d_x || !d_table || cols < 1 || !dtype_ok(x_dtype)) return fail(ABCQ_E_ARG, "abcq_lut_build: bad arguments");
+    return cuda_ret(abcq::launch_lut_build(d_x, x_dtype, cols, chunk_width, d_table, (cudaStream_t)stream),
+                    "abcq_lut_build");
+}
+
+int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes) {
+    if (int rc = check_model(m)) return rc;
+    if (!out_bytes) return fail(ABCQ_E_ARG, "out_bytes is NULL");
+    *out_bytes = m->layout == ABCQ_LAYOUT_TILED ? abcq::lut_workspace_bytes(m) : 0;
+    return 0;
+}
+
+int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y, int32_t y_dtype,
+              void* d_workspace, size_t workspace_bytes, void* stream) {
+    if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;
+    if (m->layout == ABCQ_LAYOUT_TILED) {
+        const size_t need = abcq::lut_workspace_bytes(m);
+        if (need && (!d_workspace || workspace_bytes < need))
+            return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+        return cuda_ret(abcq::launch_gemv_lut(m, p, d_x, x_dtype, d_y, y_dtype, d_workspace, (cudaStream_t)stream),
+                        "abcq_gemv");
+    }
+    return cuda_ret(abcq::launch_gemv_generic(m, p, d_x, x_dtype, d_y, y_dtype, 0, (cudaStream_t)stream),
+                    "abcq_gemv");
+}
+
+int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
+                    int32_t y_dtype, void* stream) {
+    if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;
+    return cuda_ret(abcq::launch_gemv_generic(m, p, d_x, x_dtype, d_y, y_dtype, 1, (cudaStream_t)stream),
+                    "abcq_gemv_naive");
+}
+
+int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype, void* stream) {
+    if (int rc = check_model(m)) return rc;
+    if (p < m->p_lo || p > m->p_hi)
+        return fail(ABCQ_E_PRECISION, "precision %d outside [%d, %d]", p, m->p_lo, m->p_hi);
+    if (!m->alpha[p] || (m->asymmetric && !m->offset[p])) return fail(ABCQ_E_ARG, "scale set %d missing", p);
+    if (!d_w || !dtype_ok(w_dtype)) return fail(ABCQ_E_ARG, "abcq_dequantize: bad output");
+    return cuda_ret(abcq::launch_dequantize(m, p, d_w, w_dtype, (cudaStream_t)stream), "abcq_dequantize");
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// abcq_common.cuh -- shared constants and device helpers for the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/anybcq_b200.h"
+
+namespace abcq {
+
+// ---------------------------------------------------------------------------
+// Tiled plane layout. group_size must be 128.
+//   tile  = 16 rows, slice = 256 columns (2 groups of 128 = 32 byte-chunks)
+//   block = one (slice, tile) pair of one plane = 32 lanes x 16 B = 512 B
+//   plane i, block (s, rt) at byte offset (s * NRT + rt) * 512
+//   lane l = half * 16 + r holds the 16 reference bytes of
+//       (row rt*16 + r, group 2*s + half)  -- words[i][row][4g .. 4g+3]
+//   rotated left by r: stored byte j = reference byte (j + r) & 15.
+// The rotation makes the 32 lanes of a warp touch 32 distinct table
+// columns (= 32 distinct smem banks) at every lookup step.
+// ---------------------------------------------------------------------------
+constexpr int kTileRows = 16;
+constexpr int kSliceCols = 256;
+constexpr int kGroup = 128;
+constexpr int kBlockBytes = 512;
+constexpr int kChunksPerSlice = kSliceCols / 8;  // 32
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int n_row_tiles(int rows) { return (int)ceil_div(rows, kTileRows); }
+__host__ __device__ inline int n_slices(int cols) { return (int)ceil_div(cols, kSliceCols); }
+__host__ __device__ inline int words_per_row(int cols) { return (int)ceil_div(cols, 32); }
+__host__ __device__ inline int group_count(int cols, int g) { return (int)ceil_div(cols, g); }
+
+__host__ __device__ inline int64_t tiled_plane_bytes(int rows, int cols) {
+    return (int64_t)n_slices(cols) * n_row_tiles(rows) * kBlockBytes;
+}
+// scale set p: element ((s*NRT + rt)*p + i)*32 + lane ; offsets: (s*NRT + rt)*32 + lane
+__host__ __device__ inline int64_t tiled_alpha_elems(int rows, int cols, int p) {
+    return (int64_t)n_slices(cols) * n_row_tiles(rows) * p * 32;
+}
+__host__ __device__ inline int64_t tiled_offset_elems(int rows, int cols) {
+    return (int64_t)n_slices(cols) * n_row_tiles(rows) * 32;
+}
+
+// ---------------------------------------------------------------------------
+// element load/store helpers
+// ---------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __half from_f32<__half>(float v) { return __float2half_rn(v); }
+
+__device__ __forceinline__ float load_any(const void* p, int dtype, int64_t i) {
+    return dtype == ABCQ_F16 ? __half2float(static_cast<const __half*>(p)[i])
+                             : static_cast<const float*>(p)[i];
+}
+__device__ __forceinline__ void store_any(void* p, int dtype, int64_t i, float v) {
+    if (dtype == ABCQ_F16)
+        static_cast<__half*>(p)[i] = __float2half_rn(v);
+    else
+        static_cast<float*>(p)[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// 16 entries of one mu=8 chunk of the reference lookup table (gemv.py:67-81),
+// bit-exact: the doubling concatenation gives every entry the f32 rounding
+// sequence T[t] = ((((0 -/+ x0) -/+ x1) ...) -/+ x7) in ascending j, which is
+// evaluated here directly. Entry t = hi*16 + u, u = 0..15.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void lut_chunk_entries16(const float (&xs)[8], int hi, float (&out)[16]) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        float v = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v = ((u >> j) & 1) ? v + xs[j] : v - xs[j];
+#pragma unroll
+        for (int j = 4; j < 8; ++j) v = ((hi >> (j - 4)) & 1) ? v + xs[j] : v - xs[j];
+        out[u] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// inline PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+// packed fp32x2 add (sm_100+: FADD2) -- two independent partial sums per op
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+
+// streaming 128-bit weight load: read once, keep out of L1
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+}  // namespace abcq

@@ -1,0 +1,33 @@
+// abcq_internal.h -- launcher declarations shared between the .cu files.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/anybcq_b200.h"
+
+namespace abcq {
+
+int launch_pack_planes(const uint32_t* words, int planes, int rows, int cols, void* out, cudaStream_t st);
+int launch_unpack_planes(const void* tiled, int planes, int rows, int cols, uint32_t* words, cudaStream_t st);
+int launch_pack_scales(const float* alpha, const float* offset, int p, int rows, int cols, int scale_dtype,
+                       void* alpha_out, void* offset_out, cudaStream_t st);
+int launch_lut_build(const void* x, int x_dtype, int cols, int mu, float* table, cudaStream_t st);
+
+// fast path: TILED layout, group 128
+size_t lut_workspace_bytes(const abcq_model_t* m);
+int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
+                    void* ws, cudaStream_t st);
+
+// generic path: either layout, any group size. naive=1 -> f64 per-column
+// accumulation (GemvEngine.naive), naive=0 -> f32 group sums (GemvEngine.lut)
+int launch_gemv_generic(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
+                        int naive, cudaStream_t st);
+
+int launch_dequantize(const abcq_model_t* m, int p, void* w, int w_dtype, cudaStream_t st);
+
+int num_sms();
+int probe_kernel_image();  // cudaFuncGetAttributes on a packing kernel
+
+}  // namespace abcq

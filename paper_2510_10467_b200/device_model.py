@@ -1,0 +1,262 @@
+"""GPU-resident multi-precision model: one stack of p_hi planes plus an
+independent scale set per servable precision (progressive.py:32-79), laid
+out for the sm_100a kernels.
+
+Every request picks its precision p at call time; precision p reads exactly
+planes 0..p-1 and scale set p. Planes can be uploaded progressively
+(`load_planes`): once planes 0..p-1 and set p are resident the model serves
+p, before the higher planes land (ABCQ containers store planes ascending,
+model_format.py:1-15).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import UsageError
+from .model import QuantConfig, group_count, words_per_row
+
+_SCALE_DTYPES = {"f32": (_lib.F32, torch.float32), "f16": (_lib.F16, torch.float16)}
+_TORCH_DTYPE_CODE = {torch.float32: _lib.F32, torch.float16: _lib.F16}
+
+
+def dtype_code(t: torch.dtype) -> int:
+    try:
+        return _TORCH_DTYPE_CODE[t]
+    except KeyError:
+        raise UsageError(f"unsupported dtype {t}; use float32 or float16") from None
+
+
+def require_cuda(device=None) -> torch.device:
+    """The product path has no CPU fallback: fail loudly without a GPU."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("anybcq-b200 needs a CUDA device (B200, sm_100a); none is visible. "
+                           "There is no CPU fallback.")
+    dev = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+    if dev.type != "cuda":
+        raise UsageError(f"device must be a CUDA device, got {dev}")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    _lib.check(_lib.lib().abcq_device_check(idx), "abcq_device_check")
+    return torch.device("cuda", idx)
+
+
+def _stream_handle(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class DeviceModel:
+    """Device copy of a MultiPrecisionModel in the kernels' layout.
+
+    Args:
+        rows, cols, group_size, p_lo, p_hi, asymmetric: model geometry.
+        scale_dtype: "f32" (bit-exact reference scales) or "f16" (deployment
+            width; the container's scale_width=2 rounding, model_format.py:43-52).
+        device: CUDA device.
+    """
+
+    def __init__(self, rows, cols, group_size, p_lo, p_hi, asymmetric=False, *,
+                 scale_dtype="f32", device=None):
+        if scale_dtype not in _SCALE_DTYPES:
+            raise UsageError(f"scale_dtype must be one of {sorted(_SCALE_DTYPES)}")
+        if not 1 <= p_lo <= p_hi <= _lib.ABCQ_MAX_PLANES:
+            raise UsageError(f"invalid precision range [{p_lo}, {p_hi}]")
+        self.device = require_cuda(device)
+        self.rows, self.cols, self.group_size = int(rows), int(cols), int(group_size)
+        self.p_lo, self.p_hi, self.asymmetric = int(p_lo), int(p_hi), bool(asymmetric)
+        self.groups = group_count(self.cols, self.group_size)
+        self.scale_dtype = scale_dtype
+        self._sd_code, self._sd_torch = _SCALE_DTYPES[scale_dtype]
+        self.layout = _lib.LAYOUT_TILED if self.group_size == 128 else _lib.LAYOUT_ROWMAJOR
+        L = _lib.lib()
+        if self.layout == _lib.LAYOUT_TILED:
+            pb = C.c_int64()
+            _lib.check(L.abcq_tiled_plane_bytes(self.rows, self.cols, C.byref(pb)))
+            self.plane_stride = pb.value
+        else:
+            self.plane_stride = self.rows * words_per_row(self.cols) * 4
+        self.planes = torch.zeros(self.p_hi * self.plane_stride, dtype=torch.uint8, device=self.device)
+        self.alpha: dict[int, torch.Tensor] = {}
+        self.offset: dict[int, torch.Tensor] = {}
+        self.planes_loaded = 0
+        self._ws: dict[int, torch.Tensor] = {}
+        self._struct = _lib.AbcqModel()
+        self._refresh_struct()
+
+    # ---- construction ------------------------------------------------------
+    @classmethod
+    def from_model(cls, model, *, scale_dtype="f32", device=None) -> "DeviceModel":
+        """Upload a MultiPrecisionModel (ours or the reference's, duck typed)."""
+        rows, cols = model.shape
+        cfg = model.config
+        dm = cls(rows, cols, cfg.group_size, model.p_lo, model.p_hi, cfg.asymmetric,
+                 scale_dtype=scale_dtype, device=device)
+        dm.load_planes(model.bitplanes.words)
+        for p in model.precisions:
+            st = model.scale_sets[p]
+            dm.load_scale_set(p, st.alpha, st.offset)
+        return dm
+
+    def load_planes(self, words, first: int = 0) -> None:
+        """Upload reference-layout planes words (k, rows, wpr) u32 as planes
+        first..first+k-1 (progressive loading: planes arrive ascending)."""
+        if isinstance(words, torch.Tensor):
+            w = words.to(self.device).contiguous()
+        else:
+            w = np.ascontiguousarray(words, dtype="<u4")
+            w = torch.from_numpy(w.view(np.int32)).to(self.device)
+        k = w.shape[0]
+        if w.shape[1:] != (self.rows, words_per_row(self.cols)) or not 0 <= first or first + k > self.p_hi:
+            raise UsageError(f"planes {tuple(w.shape)} at {first} do not fit a {self.p_hi}-plane "
+                             f"{self.rows}x{self.cols} model")
+        dst = self.planes[first * self.plane_stride:(first + k) * self.plane_stride]
+        with torch.cuda.device(self.device):
+            if self.layout == _lib.LAYOUT_TILED:
+                _lib.check(_lib.lib().abcq_pack_planes(
+                    w.data_ptr(), k, self.rows, self.cols, dst.data_ptr(), _stream_handle(None)),
+                    "abcq_pack_planes")
+            else:
+                dst.copy_(w.view(torch.uint8).reshape(-1))
+        self.planes_loaded = max(self.planes_loaded, first + k)
+
+    def load_scale_set(self, p: int, alpha, offset=None) -> None:
+        """Upload scale set p: alpha (p, rows, G) f32, offset (rows, G) f32 or None."""
+        if not self.p_lo <= p <= self.p_hi:
+            raise UsageError(f"precision {p} outside [{self.p_lo}, {self.p_hi}]")
+        alpha = np.ascontiguousarray(alpha, dtype=np.float32)
+        if alpha.shape != (p, self.rows, self.groups):
+            raise UsageError(f"alpha shape {alpha.shape} != {(p, self.rows, self.groups)}")
+        if (offset is not None) != self.asymmetric:
+            raise UsageError("offset presence does not match the model mode")
+        a_dev = torch.from_numpy(alpha).to(self.device)
+        o_dev = None
+        if offset is not None:
+            offset = np.ascontiguousarray(offset, dtype=np.float32)
+            if offset.shape != (self.rows, self.groups):
+                raise UsageError(f"offset shape {offset.shape} != {(self.rows, self.groups)}")
+            o_dev = torch.from_numpy(offset).to(self.device)
+        if self.layout == _lib.LAYOUT_TILED:
+            na, no = C.c_int64(), C.c_int64()
+            _lib.check(_lib.lib().abcq_tiled_scale_elems(self.rows, self.cols, p, C.byref(na), C.byref(no)))
+            a_out = torch.empty(na.value, dtype=self._sd_torch, device=self.device)
+            o_out = torch.empty(no.value, dtype=self._sd_torch, device=self.device) if o_dev is not None else None
+            with torch.cuda.device(self.device):
+                _lib.check(_lib.lib().abcq_pack_scales(
+                    a_dev.data_ptr(), _lib.ptr(o_dev), p, self.rows, self.cols, self.group_size,
+                    self._sd_code, a_out.data_ptr(), _lib.ptr(o_out), _stream_handle(None)),
+                    "abcq_pack_scales")
+        else:
+            a_out = a_dev.to(self._sd_torch).contiguous()
+            o_out = o_dev.to(self._sd_torch).contiguous() if o_dev is not None else None
+        self.alpha[p] = a_out
+        if o_out is not None:
+            self.offset[p] = o_out
+        self._refresh_struct()
+
+    def _refresh_struct(self) -> None:
+        s = self._struct
+        s.rows, s.cols, s.group_size = self.rows, self.cols, self.group_size
+        s.p_lo, s.p_hi, s.asymmetric = self.p_lo, self.p_hi, int(self.asymmetric)
+        s.layout, s.scale_dtype = self.layout, self._sd_code
+        s.plane_stride_bytes = self.plane_stride
+        s.planes = self.planes.data_ptr()
+        for p in range(_lib.ABCQ_MAX_PLANES + 1):
+            s.alpha[p] = self.alpha[p].data_ptr() if p in self.alpha else None
+            s.offset[p] = self.offset[p].data_ptr() if p in self.offset else None
+
+    # ---- queries -------------------------------------------------------------
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.rows, self.cols
+
+    @property
+    def config(self) -> QuantConfig:
+        return QuantConfig(self.group_size, "asymmetric" if self.asymmetric else "symmetric", 0)
+
+    @property
+    def precisions(self) -> range:
+        return range(self.p_lo, self.p_hi + 1)
+
+    def servable(self, p: int) -> bool:
+        return self.p_lo <= p <= self.p_hi and p <= self.planes_loaded and p in self.alpha
+
+    def _check_p(self, p: int) -> None:
+        if p not in self.precisions:
+            raise UsageError(f"precision {p} outside [{self.p_lo}, {self.p_hi}]")
+        if not self.servable(p):
+            raise UsageError(f"precision {p} not resident yet (planes loaded: {self.planes_loaded}, "
+                             f"scale sets: {sorted(self.alpha)})")
+
+    def struct_ptr(self):
+        return C.byref(self._struct)
+
+    def workspace(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Zero-filled split-K workspace, one per stream (abcq_gemv contract)."""
+        h = _stream_handle(stream)
+        ws = self._ws.get(h)
+        if ws is None:
+            n = C.c_size_t()
+            _lib.check(_lib.lib().abcq_gemv_workspace_bytes(self.struct_ptr(), C.byref(n)))
+            ws = torch.zeros(max(int(n.value), 16), dtype=torch.uint8, device=self.device)
+            self._ws[h] = ws
+        return ws
+
+    def plane_bytes(self, p: int) -> int:
+        """Bytes precision p reads from the plane stack (tiled: padded tiles)."""
+        return p * self.plane_stride
+
+    # ---- device compute ----------------------------------------------------
+    def _check_x(self, x: torch.Tensor) -> torch.Tensor:
+        if not isinstance(x, torch.Tensor) or x.device != self.device:
+            raise UsageError(f"x must be a tensor on {self.device}")
+        if x.numel() != self.cols:
+            raise UsageError(f"input length {x.numel()} != cols {self.cols}")
+        return x.contiguous()
+
+    def gemv(self, p: int, x: torch.Tensor, out: torch.Tensor | None = None,
+             out_dtype: torch.dtype = torch.float32, stream=None) -> torch.Tensor:
+        """y = W_p x on the device, asynchronous on `stream` (default: current)."""
+        self._check_p(p)
+        x = self._check_x(x)
+        if out is None:
+            out = torch.empty(self.rows, dtype=out_dtype, device=self.device)
+        elif out.numel() != self.rows or not out.is_contiguous():
+            raise UsageError("out must be a contiguous tensor of `rows` elements")
+        ws = self.workspace(stream)
+        _lib.check(_lib.lib().abcq_gemv(
+            self.struct_ptr(), p, x.data_ptr(), dtype_code(x.dtype), out.data_ptr(),
+            dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv")
+        return out
+
+    def gemv_naive(self, p: int, x: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
+        self._check_p(p)
+        x = self._check_x(x)
+        out = torch.empty(self.rows, dtype=out_dtype, device=self.device)
+        _lib.check(_lib.lib().abcq_gemv_naive(
+            self.struct_ptr(), p, x.data_ptr(), dtype_code(x.dtype), out.data_ptr(),
+            dtype_code(out.dtype), _stream_handle(stream)), "abcq_gemv_naive")
+        return out
+
+    def dequantize(self, p: int, dtype=torch.float32, stream=None) -> torch.Tensor:
+        """Dense reconstruction (rows, cols) of precision p (bcq.py:372-378)."""
+        self._check_p(p)
+        w = torch.empty(self.rows, self.cols, dtype=dtype, device=self.device)
+        _lib.check(_lib.lib().abcq_dequantize(self.struct_ptr(), p, w.data_ptr(), dtype_code(dtype),
+                                              _stream_handle(stream)), "abcq_dequantize")
+        return w
+
+    def unpack_words(self) -> torch.Tensor:
+        """Planes back in the reference layout (p_hi, rows, wpr) as int32 bits."""
+        wpr = words_per_row(self.cols)
+        out = torch.zeros(self.p_hi, self.rows, wpr, dtype=torch.int32, device=self.device)
+        if self.layout == _lib.LAYOUT_TILED:
+            _lib.check(_lib.lib().abcq_unpack_planes(
+                self.planes.data_ptr(), self.p_hi, self.rows, self.cols, out.data_ptr(),
+                _stream_handle(None)), "abcq_unpack_planes")
+        else:
+            out.view(torch.uint8).reshape(-1).copy_(self.planes)
+        return out

@@ -177,8 +177,9 @@ def run_gpu(args):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             step_launches()
-        for _ in range(args.warmup):
-            graph.replay()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                graph.replay()
         torch.cuda.synchronize()
 
     # ---- timed region: K steps, events on the launching stream ------------
@@ -217,13 +218,14 @@ def run_gpu(args):
                 with torch.cuda.graph(g2, stream=stream):
                     for j in range(reps):
                         models[j % copies][li].gemv(p, xs[k], out=ys[j % copies][li], stream=stream)
-                g2.replay()
-                torch.cuda.synchronize()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                for _ in range(5):
+                with torch.cuda.stream(stream):   # replay() launches on the current stream
                     g2.replay()
-                b.record(stream)
+                    torch.cuda.synchronize()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for _ in range(5):
+                        g2.replay()
+                    b.record(stream)
                 torch.cuda.synchronize()
                 us = a.elapsed_time(b) * 1e3 / (5 * reps)
                 per_shape[f"{name}_{r}x{k}_p{p}"] = {
@@ -232,17 +234,22 @@ def run_gpu(args):
         # cuBLAS fp16 GEMV comparator (dense fp16 weights, one copy > L2)
         dense = [torch.randn(r, k, device=dev, dtype=torch.float16) * 0.01 for _, r, k in LAYERS]
         yd = [torch.empty(r, device=dev, dtype=torch.float16) for _, r, _ in LAYERS]
+        with torch.cuda.stream(stream):
+            for li, (_, r, k) in enumerate(LAYERS):   # cuBLAS handle/workspace before capture
+                torch.mv(dense[li], xs[k], out=yd[li])
+        torch.cuda.synchronize()
         gd = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gd, stream=stream):
             for li, (_, r, k) in enumerate(LAYERS):
                 torch.mv(dense[li], xs[k], out=yd[li])
-        gd.replay()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(20):
+        with torch.cuda.stream(stream):
             gd.replay()
-        b.record(stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(20):
+                gd.replay()
+            b.record(stream)
         torch.cuda.synchronize()
         fp16_us = a.elapsed_time(b) * 1e3 / 20
         fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)

@@ -83,6 +83,14 @@ const char* abcq_last_error(void);
 /* 0 if device `dev` is sm_100 and the sm_100a kernels load, else ABCQ_E_DEVICE */
 int abcq_device_check(int32_t dev);
 
+/* profiling aid: when d_buf != NULL, every later LUT GEMV launch writes 8
+ * u64 %globaltimer stamps per CTA (phases: start, prefetch issued, PDL wait
+ * done, table built, stream done, reduction done) to d_buf[cta*8 + k].    */
+int abcq_debug_set_trace(void* d_buf);
+/* profiling experiments only (results are WRONG when mode != 0): 1 = skip
+ * the table lookups, 2 = skip the weight loads. Default 0.                */
+int abcq_debug_set_mode(int32_t mode);
+
 /* ---- layout sizes (host-only arithmetic) ---------------------------------
  * Tiled layout: 16-row tiles x 256-column slices; see DESIGN.md §Layout.  */
 int abcq_tiled_plane_bytes(int32_t rows, int32_t cols, int64_t* out_bytes);

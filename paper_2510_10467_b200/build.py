@@ -42,17 +42,23 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
-    logs = []
-    for src in sources():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src: Path):
         obj = objdir / (src.stem + ".o")
         cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
-        if r.returncode != 0:
-            sys.stderr.write(logs[-1])
+        return src, obj, r.returncode, f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}"
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    logs = [log for *_, log in results]
+    for src, _, rc, log in results:
+        if rc != 0:
+            sys.stderr.write(log)
             raise RuntimeError(f"nvcc failed on {src.name}")
-        objs.append(str(obj))
+    objs = [str(obj) for _, obj, _, _ in results]
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [_nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

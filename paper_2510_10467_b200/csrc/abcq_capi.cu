@@ -72,6 +72,16 @@ extern "C" {
 
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
+int abcq_debug_set_mode(int32_t mode) {
+    abcq::g_dbg_mode = mode;
+    return 0;
+}
+
+int abcq_debug_set_trace(void* d_buf) {
+    abcq::g_trace = static_cast<unsigned long long*>(d_buf);
+    return 0;
+}
+
 const char* abcq_last_error(void) { return g_err; }
 
 int abcq_device_check(int32_t dev) {
@@ -149,7 +159,7 @@ int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes) {
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y, int32_t y_dtype,
               void* d_workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;
-    if (m->layout == ABCQ_LAYOUT_TILED) {
+    if (abcq::lut_supports(m, p)) {
         const size_t need = abcq::lut_workspace_bytes(m);
         if (need && (!d_workspace || workspace_bytes < need))
             return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);

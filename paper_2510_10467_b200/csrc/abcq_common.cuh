@@ -35,7 +35,7 @@ __host__ __device__ inline int group_count(int cols, int g) { return (int)ceil_d
 __host__ __device__ inline int64_t tiled_plane_bytes(int rows, int cols) {
     return (int64_t)n_slices(cols) * n_row_tiles(rows) * kBlockBytes;
 }
-// scale set p: element ((s*NRT + rt)*p + i)*32 + lane ; offsets: (s*NRT + rt)*32 + lane
+// scale set p: element ((s*NRT + rt)*32 + lane)*p + i ; offsets: (s*NRT + rt)*32 + lane
 __host__ __device__ inline int64_t tiled_alpha_elems(int rows, int cols, int p) {
     return (int64_t)n_slices(cols) * n_row_tiles(rows) * p * 32;
 }
@@ -118,4 +118,57 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     return r;
 }
 
+}  // namespace abcq
+
+namespace abcq {
+// ---------------------------------------------------------------------------
+// mbarrier + bulk async copy (TMA engine, cp.async.bulk) helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+// global -> shared bulk copy through the TMA engine; completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+}  // namespace abcq
+
+namespace abcq {
+// TMA-engine prefetch of a contiguous global range into L2 (no smem, no regs)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// prefetch [src, src + bytes) in <= 64 KiB pieces; src and bytes multiples of 16
+__device__ __forceinline__ void prefetch_l2_range(const void* src, int64_t bytes) {
+    const char* p = static_cast<const char*>(src);
+    while (bytes > 0) {
+        const uint32_t n = bytes > 65536 ? 65536u : (uint32_t)bytes;
+        prefetch_l2_bulk(p, n);
+        p += n;
+        bytes -= n;
+    }
+}
 }  // namespace abcq

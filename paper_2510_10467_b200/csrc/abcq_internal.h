@@ -17,6 +17,7 @@ int launch_lut_build(const void* x, int x_dtype, int cols, int mu, float* table,
 
 // fast path: TILED layout, group 128
 size_t lut_workspace_bytes(const abcq_model_t* m);
+bool lut_supports(const abcq_model_t* m, int p);  // tiled layout and p <= 8
 int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
                     void* ws, cudaStream_t st);
 
@@ -27,6 +28,8 @@ int launch_gemv_generic(const abcq_model_t* m, int p, const void* x, int x_dtype
 
 int launch_dequantize(const abcq_model_t* m, int p, void* w, int w_dtype, cudaStream_t st);
 
+extern unsigned long long* g_trace;
+extern int g_dbg_mode;
 int num_sms();
 int probe_kernel_image();  // cudaFuncGetAttributes on a packing kernel
 

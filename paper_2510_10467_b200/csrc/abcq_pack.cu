@@ -91,10 +91,10 @@ __global__ void pack_scales_kernel(const float* __restrict__ alpha, const float*
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_alpha + n_off;
          u += (int64_t)gridDim.x * blockDim.x) {
         if (u < n_alpha) {
-            const int lane = (int)(u & 31);
-            const int64_t q = u >> 5;            // (s*NRT + rt)*p + i
-            const int i = (int)(q % p);
-            const int blk = (int)(q / p);
+            const int i = (int)(u % p);          // element ((s*NRT + rt)*32 + lane)*p + i
+            const int64_t q = u / p;
+            const int lane = (int)(q & 31);
+            const int blk = (int)(q >> 5);
             const int s = blk / NRT, rt = blk - s * NRT;
             const int row = rt * kTileRows + (lane & 15), g = 2 * s + (lane >> 4);
             float v = 0.f;

@@ -1,0 +1,90 @@
+"""Run one GEMV shape repeatedly (for ncu / quick timing on the GPU box).
+
+    python tools/gemv_probe.py --rows 14336 --cols 4096 --p 2 --iters 20
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2510_10467_b200 as P  # noqa: E402
+from oracle import anybcq_oracle as O  # noqa: E402  (synthetic input generator)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--rows", type=int, default=14336)
+ap.add_argument("--cols", type=int, default=4096)
+ap.add_argument("--p", type=int, default=2)
+ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--copies", type=int, default=4)
+a = ap.parse_args()
+
+torch.cuda.set_device(0)
+import os  # noqa: E402
+if os.environ.get("ABCQ_DBG_MODE"):
+    from paper_2510_10467_b200 import _lib
+    _lib.lib().abcq_debug_set_mode(int(os.environ["ABCQ_DBG_MODE"]))
+models = []
+for c in range(a.copies):
+    dm = P.DeviceModel(a.rows, a.cols, 128, 2, 4, scale_dtype="f16")
+    dm.load_planes(O.random_words(4, a.rows, a.cols, seed=c))
+    for p in (2, 3, 4):
+        dm.load_scale_set(p, np.full((p, a.rows, a.cols // 128), 0.05, np.float32))
+    models.append(dm)
+x = torch.randn(a.cols, device="cuda").half()
+y = torch.empty(a.rows, device="cuda", dtype=torch.float16)
+s = torch.cuda.current_stream()
+for i in range(3):
+    models[i % a.copies].gemv(a.p, x, out=y)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for i in range(a.iters):
+    models[i % a.copies].gemv(a.p, x, out=y)
+e1.record()
+torch.cuda.synchronize()
+us_eager = e0.elapsed_time(e1) * 1e3 / a.iters
+# back-to-back device time: a CUDA graph of `iters` launches (PDL edges kept)
+st = torch.cuda.Stream()
+with torch.cuda.stream(st):
+    for i in range(a.copies):
+        models[i].gemv(a.p, x, out=y, stream=st)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for i in range(a.iters):
+        models[i % a.copies].gemv(a.p, x, out=y, stream=st)
+with torch.cuda.stream(st):
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(5):
+        g.replay()
+    e1.record(st)
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / (5 * a.iters)
+G = a.cols // 128
+byts = a.p * a.rows * a.cols // 8 + a.p * a.rows * G * 2 + 2 * (a.rows + a.cols)
+print(f"{a.rows}x{a.cols} p={a.p}: graph {us:.2f} us/launch -> {byts / us / 1e3:.1f} GB/s "
+      f"(eager {us_eager:.2f} us)")
+
+if "ABCQ_TRACE" in __import__("os").environ:
+    from paper_2510_10467_b200 import _lib
+    buf = torch.zeros(148 * 8 * 4, dtype=torch.int64, device="cuda")
+    _lib.lib().abcq_debug_set_trace(buf.data_ptr())
+    with torch.cuda.stream(st):
+        for i in range(3):
+            models[i % a.copies].gemv(a.p, x, out=y, stream=st)
+    torch.cuda.synchronize()
+    _lib.lib().abcq_debug_set_trace(None)
+    t = buf.view(-1, 8)[:148].cpu().numpy().astype(np.float64)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3  # us
+    names = ["start", "prefetched", "pdl_wait", "table", "stream_done", "reduced"]
+    for k, n in enumerate(names):
+        col = rel[:, k]
+        col = col[t[:, k] > 0]
+        if len(col):
+            print(f"  {n:12s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")

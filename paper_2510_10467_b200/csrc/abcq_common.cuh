@@ -35,7 +35,8 @@ __host__ __device__ inline int group_count(int cols, int g) { return (int)ceil_d
 __host__ __device__ inline int64_t tiled_plane_bytes(int rows, int cols) {
     return (int64_t)n_slices(cols) * n_row_tiles(rows) * kBlockBytes;
 }
-// scale set p: element ((s*NRT + rt)*32 + lane)*p + i ; offsets: (s*NRT + rt)*32 + lane
+// scale set p: element (i*items + item)*32 + lane, item = s*NRT + rt, items = NS*NRT;
+// offsets: item*32 + lane
 __host__ __device__ inline int64_t tiled_alpha_elems(int rows, int cols, int p) {
     return (int64_t)n_slices(cols) * n_row_tiles(rows) * p * 32;
 }

@@ -48,7 +48,8 @@ __device__ __forceinline__ float scale_at(const GenArgs& a, int i, int n, int gr
     }
     const int NRT = n_row_tiles(a.rows);
     const int s = grp >> 1, half = grp & 1, rt = n >> 4, r = n & 15;
-    return load_any(a.alpha, a.scale_dtype, ((((int64_t)s * NRT + rt) * 32) + half * 16 + r) * a.p + i);
+    const int64_t items = (int64_t)n_slices(a.cols) * NRT;
+    return load_any(a.alpha, a.scale_dtype, ((int64_t)i * items + (int64_t)s * NRT + rt) * 32 + half * 16 + r);
 }
 
 __device__ __forceinline__ float offset_at(const GenArgs& a, int n, int grp) {

@@ -33,7 +33,10 @@ int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, vo
     a.plane_stride_u4 = m->plane_stride_bytes / 16;
     a.alpha = m->alpha[p];
     a.offset = m->asymmetric ? m->offset[p] : nullptr;
-    a.trace = g_trace;
+    // trace ring: 16 launch slots of (kTraceCtas x 8) stamps; the slot is fixed
+    // at launch (and capture) time
+    static unsigned trace_seq = 0;
+    a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
     a.dbg_mode = g_dbg_mode;
     a.x = x;
     a.y = y;

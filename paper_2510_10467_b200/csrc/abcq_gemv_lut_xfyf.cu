@@ -1,6 +1,7 @@
 // abcq_gemv_lut_xfyf.cu -- instantiation unit (x float, y float) of the LUT GEMV kernel;
 // split out so nvcc compiles the four dtype combinations in parallel.
 #include "abcq_gemv_lut.cuh"
+#include "abcq_gemv_lut_direct.cuh"
 
 namespace abcq {
 template <>

@@ -91,8 +91,9 @@ __global__ void pack_scales_kernel(const float* __restrict__ alpha, const float*
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n_alpha + n_off;
          u += (int64_t)gridDim.x * blockDim.x) {
         if (u < n_alpha) {
-            const int i = (int)(u % p);          // element ((s*NRT + rt)*32 + lane)*p + i
-            const int64_t q = u / p;
+            const int64_t per_plane = (int64_t)NS * NRT * 32;  // element (i*items + item)*32 + lane
+            const int i = (int)(u / per_plane);
+            const int64_t q = u - i * per_plane;
             const int lane = (int)(q & 31);
             const int blk = (int)(q >> 5);
             const int s = blk / NRT, rt = blk - s * NRT;

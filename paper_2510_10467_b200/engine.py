@@ -175,17 +175,29 @@ class BenchRow:
     scale_bytes: int
 
 
-def _time_device(fn, repeats: int, warmup: int = 1) -> tuple[float, float]:
-    for _ in range(warmup):
-        fn()
+def _time_device(fn, repeats: int, warmup: int = 1, inner: int = 8) -> tuple[float, float]:
+    """Median/min device microseconds per call; each sample times `inner`
+    back-to-back launches between CUDA events so host enqueue gaps do not
+    count (the reference times single calls with perf_counter, gemv.py:296-305)."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(max(warmup, 1)):  # also allocates the stream's workspace
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()  # the `inner` launches replay without host gaps
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(inner):
+            fn()
     times = []
-    for _ in range(repeats):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
-        b.synchronize()
-        times.append(a.elapsed_time(b) * 1e3)
+    with torch.cuda.stream(s):
+        g.replay()
+        for _ in range(repeats):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            g.replay()
+            b.record(s)
+            b.synchronize()
+            times.append(a.elapsed_time(b) * 1e3 / inner)
     arr = np.asarray(times)
     return float(np.median(arr)), float(arr.min())
 

@@ -19,14 +19,14 @@ def tiled_planes(words: np.ndarray, rows: int, cols: int) -> np.ndarray:
 
 
 def tiled_scales(alpha: np.ndarray, rows: int, cols: int) -> np.ndarray:
-    """alpha (p, rows, G) -> (NS, NRT, 32 lanes, p) with lane = half*16 + r."""
+    """alpha (p, rows, G) -> (p, NS, NRT, 32 lanes) with lane = half*16 + r."""
     p, _, G = alpha.shape
     nrt, ns = -(-rows // 16), -(-cols // 256)
     pad = np.zeros((p, nrt * 16, ns * 2), dtype=alpha.dtype)
     pad[:, :rows, :G] = alpha
     t = pad.reshape(p, nrt, 16, ns, 2)                                 # i, rt, r, s, half
-    return np.ascontiguousarray(t.transpose(3, 1, 4, 2, 0)).reshape(ns, nrt, 32, p)
+    return np.ascontiguousarray(t.transpose(0, 3, 1, 4, 2)).reshape(p, ns, nrt, 32)
 
 
 def tiled_offsets(offset: np.ndarray, rows: int, cols: int) -> np.ndarray:
-    return tiled_scales(offset[None], rows, cols)[..., 0]
+    return tiled_scales(offset[None], rows, cols)[0]

@@ -71,20 +71,34 @@ print(f"{a.rows}x{a.cols} p={a.p}: graph {us:.2f} us/launch -> {byts / us / 1e3:
       f"(eager {us_eager:.2f} us)")
 
 if "ABCQ_TRACE" in __import__("os").environ:
+    # timeline of 8 consecutive launches inside one CUDA graph (PDL edges kept)
     from paper_2510_10467_b200 import _lib
-    buf = torch.zeros(148 * 8 * 4, dtype=torch.int64, device="cuda")
+    SL = 160 * 8
+    buf = torch.zeros(16 * SL, dtype=torch.int64, device="cuda")
     _lib.lib().abcq_debug_set_trace(buf.data_ptr())
-    with torch.cuda.stream(st):
-        for i in range(3):
+    g3 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g3, stream=st):
+        for i in range(8):
             models[i % a.copies].gemv(a.p, x, out=y, stream=st)
-    torch.cuda.synchronize()
     _lib.lib().abcq_debug_set_trace(None)
-    t = buf.view(-1, 8)[:148].cpu().numpy().astype(np.float64)
-    t0 = t[:, 0].min()
-    rel = (t - t0) / 1e3  # us
-    names = ["start", "prefetched", "pdl_wait", "table", "stream_done", "reduced"]
-    for k, n in enumerate(names):
-        col = rel[:, k]
-        col = col[t[:, k] > 0]
-        if len(col):
-            print(f"  {n:12s} min {col.min():7.2f}  med {np.median(col):7.2f}  max {col.max():7.2f} us")
+    with torch.cuda.stream(st):
+        g3.replay()
+        torch.cuda.synchronize()
+        buf.zero_()
+        g3.replay()
+    torch.cuda.synchronize()
+    t = buf.view(16, 160, 8).cpu().numpy().astype(np.float64)
+    used = [k for k in range(16) if t[k, :, 0].max() > 0]
+    t0 = min(t[k, :148, 0][t[k, :148, 0] > 0].min() for k in used)
+    names = ["start", "prefetch", "pdl_wait", "table", "stream_done"]
+    for k in sorted(used, key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min()):
+        row = []
+        for j, n in enumerate(names):
+            col = t[k, :148, j]
+            col = col[col > 0]
+            if len(col):
+                row.append(f"{n} {((col.min() - t0) / 1e3):6.2f}/{((np.median(col) - t0) / 1e3):6.2f}/{((col.max() - t0) / 1e3):6.2f}")
+        red = t[k, 159, :3]
+        if red[0] > 0:
+            row.append("reduce " + "/".join(f"{(v - t0) / 1e3:6.2f}" for v in red))
+        print("  " + " | ".join(row))

@@ -41,6 +41,9 @@ sys.path.insert(0, str(ROOT))
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+# how a decoder layer issues them: projections that share an input run as one
+# batched launch (abcq_gemv_batch), the others alone
+GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
 P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
@@ -159,12 +162,20 @@ def run_gpu(args):
 
     stream = torch.cuda.Stream(device=dev)
 
+    from paper_2510_10467_b200.device_model import gemv_batch
+
     def step_launches():
+        for pi, p in enumerate(PRECISIONS):
+            for grp in GROUPS:
+                gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
+                if world > 1:
+                    for li in grp:
+                        dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
+
+    def single_launches():
         for pi, p in enumerate(PRECISIONS):
             for li, m in enumerate(models[pi]):
                 m.gemv(p, xs[m.cols], out=ys[pi][li], stream=stream)
-                if world > 1:
-                    dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
 
     # warm up (allocates per-stream workspaces), then capture one step as a graph
     with torch.cuda.stream(stream):
@@ -207,6 +218,27 @@ def run_gpu(args):
     ms_step = ms / args.steps
     total_bytes = step_bytes() * world
     value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # ---- the same step as 21 separate launches (one GEMV per launch) -------
+    single = None
+    if rank == 0:
+        with torch.cuda.stream(stream):
+            single_launches()
+        torch.cuda.synchronize()
+        gs = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gs, stream=stream):
+            single_launches()
+        with torch.cuda.stream(stream):
+            gs.replay()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(10):
+                gs.replay()
+            a1.record(stream)
+        torch.cuda.synchronize()
+        sms = a0.elapsed_time(a1) / 10
+        single = {"ms_per_step": round(sms, 4), "GBps": round(step_bytes() / (sms * 1e-3) / 1e9, 1)}
 
     # ---- per-shape breakdown (device time, back-to-back launches) ----------
     per_shape = {}
@@ -269,12 +301,14 @@ def run_gpu(args):
         def e2e_step():
             nonlocal h2d, d2h
             for pi, p in enumerate(PRECISIONS):
-                for li, m in enumerate(models[pi]):
-                    dx[m.cols].copy_(hx[m.cols], non_blocking=True)
-                    y = m.gemv(p, dx[m.cols], out=ys[pi][li], stream=stream)
-                    hy[pi][li].copy_(y, non_blocking=True)
-                    h2d += hx[m.cols].numel() * 2
-                    d2h += y.numel() * 2
+                for grp in GROUPS:
+                    for k in {models[pi][li].cols for li in grp}:
+                        dx[k].copy_(hx[k], non_blocking=True)
+                        h2d += hx[k].numel() * 2
+                    gemv_batch([(models[pi][li], p, dx[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
+                    for li in grp:
+                        hy[pi][li].copy_(ys[pi][li], non_blocking=True)
+                        d2h += ys[pi][li].numel() * 2
         with torch.cuda.stream(stream):
             for _ in range(3):
                 e2e_step()
@@ -290,7 +324,7 @@ def run_gpu(args):
         e2e_ms = a.elapsed_time(b) / n_e2e
         e2e = {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d // n_e2e,
-               "d2h_bytes_per_step": d2h // n_e2e, "api": "DeviceModel.gemv (C ABI abcq_gemv) per call"}
+               "d2h_bytes_per_step": d2h // n_e2e, "api": "gemv_batch per decoder group (C ABI abcq_gemv_batch / abcq_gemv), host x/y"}
 
     if rank == 0:
         peak, peak_kind = read_peaks()
@@ -310,14 +344,18 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
             "config": {"workload": "Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, "
-                                   "p=2,3,4 per step, g=128, fp16 scales/x/y",
+                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; launches grouped as a "
+                                   "decoder issues them: [q,k,v] [o] [gate,up] [down]",
                        "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
                              f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
                        "timing": "CUDA graph of one step, CUDA events on the launch stream",
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
-            "gpu_launches": args.steps * len(LAYERS) * len(PRECISIONS),
+            # per p: 4 group launches + a split-reduce kernel after each single-job
+            # group whose K spans > 1 slice (o, down)
+            "gpu_launches": args.steps * len(PRECISIONS) * (len(GROUPS) + 2),
+            "single_launch_per_gemv": single,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_kind": peak_kind,

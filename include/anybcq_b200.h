@@ -133,6 +133,27 @@ int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
               int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ---- batches of independent GEMVs ----------------------------------------
+ * One persistent launch runs n_jobs GemvEngine.lut calls back to back (the
+ * TMA stream never drains between them) -- e.g. q/k/v or gate/up of a
+ * decoder layer, or several requests' precisions. All jobs: TILED layout,
+ * the same x/y/scale dtypes and mode; n_jobs <= abcq_gemv_batch_max_jobs().
+ * Workspace: abcq_gemv_batch_workspace_bytes, zero-filled once per stream
+ * AND per job-list layout (it holds self-resetting counters at offsets that
+ * depend on the jobs' shapes).                                              */
+typedef struct abcq_gemv_job {
+    const abcq_model_t* model;
+    int32_t p;
+    int32_t x_dtype;
+    int32_t y_dtype;
+    const void* x; /* device (cols) */
+    void* y;       /* device (rows) */
+} abcq_gemv_job_t;
+int abcq_gemv_batch_max_jobs(void);
+int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n_jobs, size_t* out_bytes);
+int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n_jobs, void* d_workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* ---- naive path: replaces GemvEngine.naive (gemv.py:170-186) ------------
  * Column-by-column decode of the planes (either layout, any group size).   */
 int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype,

@@ -43,8 +43,22 @@ class AbcqModel(C.Structure):
     ]
 
 
+class AbcqGemvJob(C.Structure):
+    """Mirror of `abcq_gemv_job_t` (include/anybcq_b200.h)."""
+
+    _fields_ = [
+        ("model", C.POINTER(AbcqModel)),
+        ("p", C.c_int32),
+        ("x_dtype", C.c_int32),
+        ("y_dtype", C.c_int32),
+        ("x", C.c_void_p),
+        ("y", C.c_void_p),
+    ]
+
+
 _vp, _i32, _i64, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
 _PM = C.POINTER(AbcqModel)
+_PJ = C.POINTER(AbcqGemvJob)
 
 # name -> (restype, argtypes); every symbol declared in the header
 SIGNATURES = {
@@ -62,6 +76,9 @@ SIGNATURES = {
     "abcq_gemv_workspace_bytes": (C.c_int, [_PM, C.POINTER(_sz)]),
     "abcq_gemv": (C.c_int, [_PM, _i32, _vp, _i32, _vp, _i32, _vp, _sz, _vp]),
     "abcq_gemv_naive": (C.c_int, [_PM, _i32, _vp, _i32, _vp, _i32, _vp]),
+    "abcq_gemv_batch_max_jobs": (C.c_int, []),
+    "abcq_gemv_batch_workspace_bytes": (C.c_int, [_PJ, _i32, C.POINTER(_sz)]),
+    "abcq_gemv_batch": (C.c_int, [_PJ, _i32, _vp, _sz, _vp]),
     "abcq_dequantize": (C.c_int, [_PM, _i32, _vp, _i32, _vp]),
 }
 

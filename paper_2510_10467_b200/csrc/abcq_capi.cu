@@ -170,6 +170,53 @@ int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype
                     "abcq_gemv");
 }
 
+int abcq_gemv_batch_max_jobs(void) { return abcq::lut_max_jobs(); }
+
+static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {
+    if (!jobs || n < 1) return fail(ABCQ_E_ARG, "empty job list");
+    if (n > abcq::lut_max_jobs()) return fail(ABCQ_E_ARG, "%d jobs > max %d", n, abcq::lut_max_jobs());
+    const abcq_model_t* m0 = jobs[0].model;
+    for (int j = 0; j < n; ++j) {
+        const abcq_gemv_job_t& J = jobs[j];
+        if (int rc = check_call(J.model, J.p, J.x, J.x_dtype, J.y, J.y_dtype)) return rc;
+        if (!abcq::lut_supports(J.model, J.p))
+            return fail(ABCQ_E_LAYOUT, "job %d: batched GEMV needs the tiled layout (group 128)", j);
+        if (J.x_dtype != jobs[0].x_dtype || J.y_dtype != jobs[0].y_dtype ||
+            J.model->scale_dtype != m0->scale_dtype || J.model->asymmetric != m0->asymmetric)
+            return fail(ABCQ_E_ARG, "job %d: dtypes / mode differ from job 0", j);
+    }
+    return 0;
+}
+
+int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n, size_t* out_bytes) {
+    if (int rc = check_jobs(jobs, n)) return rc;
+    if (!out_bytes) return fail(ABCQ_E_ARG, "out_bytes is NULL");
+    size_t tot = 0;
+    for (int j = 0; j < n; ++j) tot += abcq::lut_workspace_bytes(jobs[j].model);
+    *out_bytes = tot;
+    return 0;
+}
+
+int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t ws_bytes, void* stream) {
+    size_t need = 0;
+    if (int rc = abcq_gemv_batch_workspace_bytes(jobs, n, &need)) return rc;
+    if (need && (!d_ws || ws_bytes < need))
+        return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    const abcq_model_t* models[ABCQ_MAX_PLANES + 16];
+    int ps[ABCQ_MAX_PLANES + 16];
+    const void* xs[ABCQ_MAX_PLANES + 16];
+    void* ys[ABCQ_MAX_PLANES + 16];
+    for (int j = 0; j < n; ++j) {
+        models[j] = jobs[j].model;
+        ps[j] = jobs[j].p;
+        xs[j] = jobs[j].x;
+        ys[j] = jobs[j].y;
+    }
+    return cuda_ret(abcq::launch_gemv_jobs(models, ps, xs, ys, n, jobs[0].x_dtype, jobs[0].y_dtype, d_ws,
+                                           (cudaStream_t)stream),
+                    "abcq_gemv_batch");
+}
+
 int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
                     int32_t y_dtype, void* stream) {
     if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;

@@ -1,54 +1,80 @@
-// abcq_gemv_lut.cu -- launcher of the sm_100a batch-1 GEMV (kernel: abcq_gemv_lut.cuh).
-#include "abcq_gemv_lut.cuh"
+// abcq_gemv_lut.cu -- host launchers of the sm_100a LUT GEMV (kernel:
+// abcq_gemv_batch.cuh): single GEMV (abcq_gemv) and batches of independent
+// GEMVs (abcq_gemv_batch) share one persistent, warp-specialised kernel.
+#include "abcq_gemv_batch.cuh"
 
 namespace abcq {
-
-size_t lut_workspace_bytes(const abcq_model_t* m) {
-    const int NRT = n_row_tiles(m->rows), NS = n_slices(m->cols);
-    if (NS <= 1) return 0;
-    return (size_t)NS * NRT * kTileRows * sizeof(float);
-}
-
-bool lut_supports(const abcq_model_t* m, int p) { return m->layout == ABCQ_LAYOUT_TILED && p <= kMaxFastP; }
-
-template <typename XT>
-static int launch_yt(const LutArgs& a, int yd, int sd, bool asym, int grid, cudaStream_t st) {
-    return yd == ABCQ_F16 ? launch_lut_xy<XT, __half>(a, sd, asym, grid, st)
-                          : launch_lut_xy<XT, float>(a, sd, asym, grid, st);
-}
 
 unsigned long long* g_trace = nullptr;  // abcq_debug_set_trace (profiling aid)
 int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experiments)
 
-int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
-                    void* ws, cudaStream_t st) {
-    LutArgs a;
-    a.rows = m->rows;
-    a.cols = m->cols;
-    a.NRT = n_row_tiles(m->rows);
-    a.NS = n_slices(m->cols);
-    a.p = p;
-    a.items = a.NRT * a.NS;
-    a.planes = static_cast<const uint4*>(m->planes);
-    a.plane_stride_u4 = m->plane_stride_bytes / 16;
-    a.alpha = m->alpha[p];
-    a.offset = m->asymmetric ? m->offset[p] : nullptr;
-    // trace ring: 16 launch slots of (kTraceCtas x 8) stamps; the slot is fixed
-    // at launch (and capture) time
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+size_t lut_workspace_bytes(const abcq_model_t* m) {
+    const int NRT = n_row_tiles(m->rows), NS = n_slices(m->cols);
+    if (NS <= 1) return 0;
+    return align256((size_t)NS * NRT * kTileRows * sizeof(float)) + align256((size_t)NRT * sizeof(uint32_t));
+}
+
+bool lut_supports(const abcq_model_t* m, int p) {
+    return m->layout == ABCQ_LAYOUT_TILED && p <= kMaxFastP && n_slices(m->cols) <= num_sms();
+}
+
+int lut_max_jobs() { return kMaxJobs; }
+
+// fill a Job from a model + call; ws points at this job's workspace region
+static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* y, char* ws, int grid) {
+    J.rows = m->rows;
+    J.cols = m->cols;
+    J.NRT = n_row_tiles(m->rows);
+    J.NS = n_slices(m->cols);
+    J.p = p;
+    J.items = J.NRT * J.NS;
+    J.q = J.items / grid;
+    J.rem = J.items % grid;
+    J.planes = static_cast<const uint4*>(m->planes);
+    J.plane_stride_u4 = m->plane_stride_bytes / 16;
+    J.alpha = m->alpha[p];
+    J.offset = m->asymmetric ? m->offset[p] : nullptr;
+    J.x = x;
+    J.y = y;
+    J.partial = reinterpret_cast<float*>(ws);
+    J.counters = ws ? reinterpret_cast<uint32_t*>(
+                          ws + align256((size_t)J.NS * J.NRT * kTileRows * sizeof(float)))
+                    : nullptr;
+}
+
+template <typename XT>
+static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cudaStream_t st) {
+    return yd == ABCQ_F16 ? launch_batch_xy_inst<XT, __half>(a, sd, asym, grid, st)
+                          : launch_batch_xy_inst<XT, float>(a, sd, asym, grid, st);
+}
+
+int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
+                     int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st) {
+    BatchArgs a;  // passed by value (kernel parameter space)
+    const int grid = num_sms();
+    char* w = static_cast<char*>(ws);
+    for (int j = 0; j < n; ++j) {
+        make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w, grid);
+        w += lut_workspace_bytes(models[j]);
+    }
+    a.n_jobs = n;
+    // a batch pays the split-K tail once, in-kernel; a single GEMV hands it to
+    // a PDL-chained reduce kernel (shorter critical path, measured)
+    a.fused = (n > 1 && g_dbg_mode != 20) || g_dbg_mode == 21;
+    a.dbg = g_dbg_mode == 1 ? 1 : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
-    a.dbg_mode = g_dbg_mode;
-    a.x = x;
-    a.y = y;
-    a.partial = static_cast<float*>(ws);
-    int grid = num_sms();
-    if (grid < a.NS) grid = a.NS;      // keeps every CTA within <= 2 slices
-    if (grid > a.items) grid = a.items;
-    a.q = a.items / grid;
-    a.rem = a.items % grid;
+    const abcq_model_t* m = models[0];
     const bool asym = m->asymmetric != 0;
     return x_dtype == ABCQ_F16 ? launch_yt<__half>(a, y_dtype, m->scale_dtype, asym, grid, st)
                                : launch_yt<float>(a, y_dtype, m->scale_dtype, asym, grid, st);
+}
+
+int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
+                    void* ws, cudaStream_t st) {
+    return launch_gemv_jobs(&m, &p, &x, &y, 1, x_dtype, y_dtype, ws, st);
 }
 
 }  // namespace abcq

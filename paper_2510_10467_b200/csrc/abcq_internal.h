@@ -20,6 +20,11 @@ size_t lut_workspace_bytes(const abcq_model_t* m);
 bool lut_supports(const abcq_model_t* m, int p);  // tiled layout and p <= 8
 int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
                     void* ws, cudaStream_t st);
+// batch of n independent GEMVs (same dtypes / mode), workspaces concatenated
+// in job order (lut_workspace_bytes each)
+int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
+                     int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st);
+int lut_max_jobs();
 
 // generic path: either layout, any group size. naive=1 -> f64 per-column
 // accumulation (GemvEngine.naive), naive=0 -> f32 group sums (GemvEngine.lut)

@@ -260,3 +260,52 @@ class DeviceModel:
         else:
             out.view(torch.uint8).reshape(-1).copy_(self.planes)
         return out
+
+
+_BATCH_WS: dict = {}
+
+
+def gemv_batch(jobs, stream=None):
+    """Run independent GEMVs in ONE persistent launch (abcq_gemv_batch).
+
+    jobs: list of (DeviceModel, p, x, out) with x (cols,) and out (rows,)
+    CUDA tensors; all models tiled (group 128), same x/out dtypes, scale dtype
+    and mode. The same model may appear several times (e.g. one request per
+    precision). Asynchronous on `stream`; returns the list of outputs.
+    """
+    n = len(jobs)
+    L = _lib.lib()
+    if n == 0:
+        return []
+    if n > L.abcq_gemv_batch_max_jobs():
+        outs = []
+        step = L.abcq_gemv_batch_max_jobs()
+        for i in range(0, n, step):
+            outs += gemv_batch(jobs[i:i + step], stream)
+        return outs
+    arr = (_lib.AbcqGemvJob * n)()
+    keep = []
+    for k, (dm, p, x, out) in enumerate(jobs):
+        dm._check_p(p)
+        x = dm._check_x(x)
+        if out.numel() != dm.rows or not out.is_contiguous() or out.device != dm.device:
+            raise UsageError("out must be a contiguous device tensor of `rows` elements")
+        keep.append(x)
+        arr[k].model = C.pointer(dm._struct)
+        arr[k].p = p
+        arr[k].x_dtype = dtype_code(x.dtype)
+        arr[k].y_dtype = dtype_code(out.dtype)
+        arr[k].x = x.data_ptr()
+        arr[k].y = out.data_ptr()
+    need = C.c_size_t()
+    _lib.check(L.abcq_gemv_batch_workspace_bytes(arr, n, C.byref(need)), "abcq_gemv_batch")
+    dev = jobs[0][0].device
+    # the workspace holds per-job partials + self-resetting arrival counters at
+    # offsets that depend on the job list: one zero-filled buffer per layout
+    key = (_stream_handle(stream), dev.index, tuple((j[0].rows, j[0].cols) for j in jobs))
+    ws = _BATCH_WS.get(key)
+    if ws is None or ws.numel() < need.value:
+        ws = torch.zeros(max(int(need.value), 16), dtype=torch.uint8, device=dev)
+        _BATCH_WS[key] = ws
+    _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv_batch")
+    return [j[3] for j in jobs]

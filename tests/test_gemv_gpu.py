@@ -256,3 +256,35 @@ def test_bench_counters_and_render(P):
     assert len(csv.splitlines()) == len(rows) + 1
     with pytest.raises(P.UsageError):
         P.bench(make_model(P, c), [2], c["x_0"], repeats=0)
+
+
+def test_gemv_batch_matches_single_calls(P):
+    """One persistent launch over mixed shapes / precisions (incl. the same model
+    at several p, as per-request precision does) == separate calls, bitwise."""
+    from paper_2510_10467_b200.device_model import gemv_batch
+    shapes = [(4096, 4096), (1024, 4096), (14336, 4096), (4096, 14336), (37, 200), (16, 256)]
+    models = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r + c), scale_dtype="f16") for r, c in shapes]
+    xs = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for _, c in shapes}
+    jobs, want = [], []
+    for k, dm in enumerate(models):
+        for p in ((2, 4) if k == 0 else (2 + k % 3,)):
+            jobs.append((dm, p, xs[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16)))
+            want.append(dm.gemv(p, xs[dm.cols], out_dtype=torch.float16).clone())
+    gemv_batch(jobs)
+    torch.cuda.synchronize()
+    for (dm, p, _, out), w in zip(jobs, want):
+        assert torch.equal(out, w), (dm.rows, dm.cols, p)
+    gemv_batch(jobs)  # counters self-reset: a second run is identical
+    torch.cuda.synchronize()
+    for (_, _, _, out), w in zip(jobs, want):
+        assert torch.equal(out, w)
+
+
+def test_gemv_batch_asymmetric(P):
+    from paper_2510_10467_b200.device_model import gemv_batch
+    ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]
+    x = torch.from_numpy(O.random_gaussian(1, 1024, seed=3).ravel()).cuda()
+    jobs = [(m, p, x, torch.empty(m.rows, device="cuda")) for m in ms for p in (2, 3)]
+    gemv_batch(jobs)
+    for m, p, _, out in jobs:
+        assert torch.equal(out, m.gemv(p, x))

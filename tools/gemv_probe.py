@@ -79,7 +79,11 @@ if "ABCQ_TRACE" in __import__("os").environ:
     g3 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g3, stream=st):
         for i in range(8):
-            models[i % a.copies].gemv(a.p, x, out=y, stream=st)
+            if __import__("os").environ.get("ABCQ_BATCH"):
+                from paper_2510_10467_b200.device_model import gemv_batch
+                gemv_batch([(models[(i + k) % a.copies], a.p, x, y) for k in range(int(__import__("os").environ["ABCQ_BATCH"]))], st)
+            else:
+                models[i % a.copies].gemv(a.p, x, out=y, stream=st)
     _lib.lib().abcq_debug_set_trace(None)
     with torch.cuda.stream(st):
         g3.replay()
@@ -90,7 +94,7 @@ if "ABCQ_TRACE" in __import__("os").environ:
     t = buf.view(16, 160, 8).cpu().numpy().astype(np.float64)
     used = [k for k in range(16) if t[k, :, 0].max() > 0]
     t0 = min(t[k, :148, 0][t[k, :148, 0] > 0].min() for k in used)
-    names = ["start", "prefetch", "pdl_wait", "table", "stream_done"]
+    names = ["start", "tab0", "str0", "tab1", "str1", "tab2", "str2", "reduced"]
     for k in sorted(used, key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min()):
         row = []
         for j, n in enumerate(names):
@@ -102,3 +106,27 @@ if "ABCQ_TRACE" in __import__("os").environ:
         if red[0] > 0:
             row.append("reduce " + "/".join(f"{(v - t0) / 1e3:6.2f}" for v in red))
         print("  " + " | ".join(row))
+
+if __import__("os").environ.get("ABCQ_BATCH"):
+    # one persistent launch over ABCQ_BATCH jobs (rotating over the copies)
+    from paper_2510_10467_b200.device_model import gemv_batch
+    nb = int(__import__("os").environ["ABCQ_BATCH"])
+    outs = [torch.empty(a.rows, device="cuda", dtype=torch.float16) for _ in range(nb)]
+    jobs = [(models[i % a.copies], a.p, x, outs[i]) for i in range(nb)]
+    with torch.cuda.stream(st):
+        gemv_batch(jobs, st)
+    torch.cuda.synchronize()
+    gb = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gb, stream=st):
+        for _ in range(4):
+            gemv_batch(jobs, st)
+    with torch.cuda.stream(st):
+        gb.replay()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(5):
+            gb.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / 20
+    print(f"  batch of {nb}: {us:.2f} us/launch -> {nb * byts / us / 1e3:.1f} GB/s ({us / nb:.2f} us/GEMV)")

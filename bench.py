@@ -41,9 +41,12 @@ sys.path.insert(0, str(ROOT))
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-# how a decoder layer issues them: projections that share an input run as one
-# batched launch (abcq_gemv_batch), the others alone
-GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
+# The timed step runs, per precision, the 7 independent GEMVs of the sweep as
+# ONE persistent batched launch (abcq_gemv_batch). Also reported: the same
+# step grouped as a decoder issues it ([q,k,v] [o] [gate,up] [down]) and as
+# 21 single-GEMV launches.
+STEP_GROUPS = [tuple(range(7))]
+DECODER_GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
 P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
@@ -164,18 +167,39 @@ def run_gpu(args):
 
     from paper_2510_10467_b200.device_model import gemv_batch
 
-    def step_launches():
+    def grouped_launches(groups):
         for pi, p in enumerate(PRECISIONS):
-            for grp in GROUPS:
+            for grp in groups:
                 gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
                 if world > 1:
                     for li in grp:
                         dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
 
+    def step_launches():
+        grouped_launches(STEP_GROUPS)
+
     def single_launches():
         for pi, p in enumerate(PRECISIONS):
             for li, m in enumerate(models[pi]):
                 m.gemv(p, xs[m.cols], out=ys[pi][li], stream=stream)
+
+    def time_graph(fn, reps=10):
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        with torch.cuda.stream(stream):
+            g.replay()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            a1.record(stream)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / reps
 
     # warm up (allocates per-stream workspaces), then capture one step as a graph
     with torch.cuda.stream(stream):
@@ -219,26 +243,13 @@ def run_gpu(args):
     total_bytes = step_bytes() * world
     value = total_bytes / (ms_step * 1e-3) / 1e9
 
-    # ---- the same step as 21 separate launches (one GEMV per launch) -------
-    single = None
+    # ---- the same step issued as a decoder would, and as 21 single launches --
+    variants = {}
     if rank == 0:
-        with torch.cuda.stream(stream):
-            single_launches()
-        torch.cuda.synchronize()
-        gs = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gs, stream=stream):
-            single_launches()
-        with torch.cuda.stream(stream):
-            gs.replay()
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for _ in range(10):
-                gs.replay()
-            a1.record(stream)
-        torch.cuda.synchronize()
-        sms = a0.elapsed_time(a1) / 10
-        single = {"ms_per_step": round(sms, 4), "GBps": round(step_bytes() / (sms * 1e-3) / 1e9, 1)}
+        for name, fn in (("decoder_grouped", lambda: grouped_launches(DECODER_GROUPS)),
+                         ("single_launch_per_gemv", single_launches)):
+            vms = time_graph(fn)
+            variants[name] = {"ms_per_step": round(vms, 4), "GBps": round(step_bytes() / (vms * 1e-3) / 1e9, 1)}
 
     # ---- per-shape breakdown (device time, back-to-back launches) ----------
     per_shape = {}
@@ -301,7 +312,7 @@ def run_gpu(args):
         def e2e_step():
             nonlocal h2d, d2h
             for pi, p in enumerate(PRECISIONS):
-                for grp in GROUPS:
+                for grp in STEP_GROUPS:
                     for k in {models[pi][li].cols for li in grp}:
                         dx[k].copy_(hx[k], non_blocking=True)
                         h2d += hx[k].numel() * 2
@@ -344,18 +355,17 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
             "config": {"workload": "Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, "
-                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; launches grouped as a "
-                                   "decoder issues them: [q,k,v] [o] [gate,up] [down]",
+                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; per p the 7 independent "
+                                   "GEMVs run as one persistent batched launch",
                        "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
                              f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
                        "timing": "CUDA graph of one step, CUDA events on the launch stream",
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
-            # per p: 4 group launches + a split-reduce kernel after each single-job
-            # group whose K spans > 1 slice (o, down)
-            "gpu_launches": args.steps * len(PRECISIONS) * (len(GROUPS) + 2),
-            "single_launch_per_gemv": single,
+            # per p: one persistent batched launch (split-K completed in-kernel)
+            "gpu_launches": args.steps * len(PRECISIONS) * len(STEP_GROUPS),
+            "step_variants": variants,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_kind": peak_kind,

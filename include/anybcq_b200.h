@@ -154,6 +154,18 @@ int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n_jobs,
 int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n_jobs, void* d_workspace, size_t workspace_bytes,
                     void* stream);
 
+/* ---- small-batch GEMM with per-request precision --------------------------
+ * Replaces the reference's per-request loop (cli.py:122-126 loops
+ * GemvEngine.lut over the rows of x; service/server.py:188-206 serves one
+ * precision per request): Y[b] = W_{p_b} X[b] for B <= 16 requests in ONE pass
+ * over planes 0..max(p_b)-1 (tensor cores, f16 x, f32 accumulate).
+ * d_x: (B, cols) fp16; d_y: (B, rows) in y_dtype; p_host: B precisions
+ * (host array). TILED layout only.                                          */
+int abcq_gemm_mixedp_max_batch(void);
+int abcq_gemm_mixedp_workspace_bytes(const abcq_model_t* m, int32_t batch, size_t* out_bytes);
+int abcq_gemm_mixedp(const abcq_model_t* m, int32_t batch, const int32_t* p_host, const void* d_x, void* d_y,
+                     int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* ---- naive path: replaces GemvEngine.naive (gemv.py:170-186) ------------
  * Column-by-column decode of the planes (either layout, any group size).   */
 int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype,

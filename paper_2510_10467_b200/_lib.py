@@ -79,6 +79,9 @@ SIGNATURES = {
     "abcq_gemv_batch_max_jobs": (C.c_int, []),
     "abcq_gemv_batch_workspace_bytes": (C.c_int, [_PJ, _i32, C.POINTER(_sz)]),
     "abcq_gemv_batch": (C.c_int, [_PJ, _i32, _vp, _sz, _vp]),
+    "abcq_gemm_mixedp_max_batch": (C.c_int, []),
+    "abcq_gemm_mixedp_workspace_bytes": (C.c_int, [_PM, _i32, C.POINTER(_sz)]),
+    "abcq_gemm_mixedp": (C.c_int, [_PM, _i32, C.POINTER(_i32), _vp, _vp, _i32, _vp, _sz, _vp]),
     "abcq_dequantize": (C.c_int, [_PM, _i32, _vp, _i32, _vp]),
 }
 

@@ -217,6 +217,39 @@ int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t w
                     "abcq_gemv_batch");
 }
 
+int abcq_gemm_mixedp_max_batch(void) { return 16; }
+
+static int check_gemm(const abcq_model_t* m, int32_t B, const int32_t* p_host) {
+    if (int rc = check_model(m)) return rc;
+    if (m->layout != ABCQ_LAYOUT_TILED) return fail(ABCQ_E_LAYOUT, "mixed-p GEMM needs the tiled layout (group 128)");
+    if (B < 1 || B > 16) return fail(ABCQ_E_ARG, "batch %d outside [1, 16]", B);
+    if (!p_host) return fail(ABCQ_E_ARG, "p_host is NULL");
+    for (int b = 0; b < B; ++b) {
+        const int p = p_host[b];
+        if (p < m->p_lo || p > m->p_hi)
+            return fail(ABCQ_E_PRECISION, "request %d: precision %d outside [%d, %d]", b, p, m->p_lo, m->p_hi);
+        if (!m->alpha[p] || (m->asymmetric && !m->offset[p])) return fail(ABCQ_E_ARG, "scale set %d missing", p);
+    }
+    return 0;
+}
+
+int abcq_gemm_mixedp_workspace_bytes(const abcq_model_t* m, int32_t B, size_t* out_bytes) {
+    if (int rc = check_model(m)) return rc;
+    if (B < 1 || B > 16 || !out_bytes) return fail(ABCQ_E_ARG, "bad batch / out pointer");
+    *out_bytes = abcq::gemm_workspace_bytes(m, B);
+    return 0;
+}
+
+int abcq_gemm_mixedp(const abcq_model_t* m, int32_t B, const int32_t* p_host, const void* d_x, void* d_y,
+                     int32_t y_dtype, void* d_ws, size_t ws_bytes, void* stream) {
+    if (int rc = check_gemm(m, B, p_host)) return rc;
+    if (!d_x || !d_y || !dtype_ok(y_dtype)) return fail(ABCQ_E_ARG, "bad x / y");
+    const size_t need = abcq::gemm_workspace_bytes(m, B);
+    if (!d_ws || ws_bytes < need) return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return cuda_ret(abcq::launch_gemm_mixedp(m, B, p_host, d_x, d_y, y_dtype, d_ws, (cudaStream_t)stream),
+                    "abcq_gemm_mixedp");
+}
+
 int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
                     int32_t y_dtype, void* stream) {
     if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;

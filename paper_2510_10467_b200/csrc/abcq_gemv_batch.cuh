@@ -227,6 +227,21 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         rb[k] = v | ((kTableWindow >> 16) << 24);  // byte 3 -> address byte 2
     }
 
+    // x values of this thread's table tasks (chunk tid&31 of up to 2 slices)
+    static_assert(kBThreads == 512, "table build maps one thread to (chunk, hi) of a slice");
+    float xpre[2][8];
+    int xpre_job = -1;
+    auto prefetch_x = [&](int jn) {
+        const Job& Jn = a.jobs[jn];
+        const int it0 = b * Jn.q + min(b, Jn.rem);
+        const int sn = Jn.NRT > 0 ? it0 / Jn.NRT : 0;
+        const XT* __restrict__ xn = static_cast<const XT*>(Jn.x);
+#pragma unroll
+        for (int ts = 0; ts < 2; ++ts)  // slice sn + 1 may not exist: load_x8 zero-fills past cols
+            load_x8<XT>(xn, (sn + ts) * kSliceCols + 8 * (tid & 31), Jn.cols, xpre[ts]);
+        xpre_job = jn;
+    };
+
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
     for (int j = 0; j < a.n_jobs; ++j) {
         const Job& J = a.jobs[j];
@@ -236,21 +251,30 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         const int s0 = wr.s0;
         const int nseg = it1 > min((s0 + 1) * J.NRT, it1) ? 2 : 1;
         // ---- lookup tables of job j's slices (one CTA barrier each side) ------
+        // thread (c, hi) of task ts builds 16 entries of chunk c from 8 x values;
+        // they were prefetched into registers while the previous job streamed
+        if (xpre_job != j) prefetch_x(j);
         if (j > 0) __syncthreads();  // every warp is done with the previous table
-        const XT* __restrict__ x = static_cast<const XT*>(J.x);
-        const int k0 = s0 * kSliceCols;
-        for (int task = tid; task < nseg * 32 * 16; task += kBThreads) {
-            const int ts = task >> 9, c = task & 31, hi = (task >> 5) & 15;
-            float xv[8];
-            load_x8<XT>(x, k0 + ts * kSliceCols + 8 * c, J.cols, xv);
-            float ev[16];
-            lut_chunk_entries16(xv, hi, ev);
-            float* col = table + ts * 32 + c;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) col[(hi * 16 + t) * 64] = ev[t];
-            if (ASYM && hi == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
+        for (int ts = 0; ts < 2; ++ts) {
+            if (ts < nseg) {
+                const int c = tid & 31, hi = tid >> 5;
+                float ev[16];
+                lut_chunk_entries16(xpre[ts], hi, ev);
+                float* col = table + ts * 32 + c;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) col[(hi * 16 + t) * 64] = ev[t];
+                if (ASYM && hi == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
+            }
         }
         __syncthreads();
+        for (int jn = j + 1; jn < a.n_jobs; ++jn) {  // x of the next job this CTA works on
+            const Job& Jn = a.jobs[jn];
+            if (Jn.q + (b < Jn.rem ? 1 : 0) > 0) {
+                prefetch_x(jn);
+                break;
+            }
+        }
         if (j < 3 && warp == 0) ABCQ_BTRACE(1 + 2 * j);
         if (wr.n() == 0) continue;
         float gx = 0.f;

@@ -26,6 +26,11 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                      int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st);
 int lut_max_jobs();
 
+// small-batch mixed-precision GEMM (tensor cores), B <= 16
+size_t gemm_workspace_bytes(const abcq_model_t* m, int B);
+int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const void* x, void* y, int y_dtype,
+                       void* ws, cudaStream_t st);
+
 // generic path: either layout, any group size. naive=1 -> f64 per-column
 // accumulation (GemvEngine.naive), naive=0 -> f32 group sums (GemvEngine.lut)
 int launch_gemv_generic(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,

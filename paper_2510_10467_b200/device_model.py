@@ -232,6 +232,30 @@ class DeviceModel:
             dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv")
         return out
 
+    def gemm_mixedp(self, ps, X: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
+        """Y[b] = W_{ps[b]} X[b] for B <= 16 requests in one pass over the planes
+        (tensor cores). X: (B, cols) CUDA tensor (cast to fp16); returns (B, rows)."""
+        B = len(ps)
+        if X.dim() != 2 or X.shape[0] != B or X.shape[1] != self.cols:
+            raise UsageError(f"X must be ({B}, {self.cols}), got {tuple(X.shape)}")
+        for p in ps:
+            self._check_p(int(p))
+        xh = X.to(device=self.device, dtype=torch.float16).contiguous()
+        out = torch.empty(B, self.rows, dtype=out_dtype, device=self.device)
+        need = C.c_size_t()
+        L = _lib.lib()
+        _lib.check(L.abcq_gemm_mixedp_workspace_bytes(self.struct_ptr(), B, C.byref(need)), "abcq_gemm_mixedp")
+        key = ("gemm", _stream_handle(stream))
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < need.value:
+            ws = torch.empty(max(int(need.value), 16), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        parr = (C.c_int32 * B)(*[int(p) for p in ps])
+        _lib.check(L.abcq_gemm_mixedp(self.struct_ptr(), B, parr, xh.data_ptr(), out.data_ptr(),
+                                      dtype_code(out_dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)),
+                   "abcq_gemm_mixedp")
+        return out
+
     def gemv_naive(self, p: int, x: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
         self._check_p(p)
         x = self._check_x(x)

@@ -288,3 +288,23 @@ def test_gemv_batch_asymmetric(P):
     gemv_batch(jobs)
     for m, p, _, out in jobs:
         assert torch.equal(out, m.gemv(p, x))
+
+
+@pytest.mark.parametrize("asym", [False, True])
+@pytest.mark.parametrize("rows,cols", [(64, 256), (37, 200), (4096, 4096), (1024, 14336)])
+def test_gemm_mixedp_matches_per_request_oracle(P, rows, cols, asym):
+    """B <= 16 requests with mixed precision in one tensor-core pass == the
+    reference's per-request loop (cli.py:122-126) on the oracle."""
+    m = synth_model(P, rows, cols, 2, 4, asym=asym, seed=rows * 7 + cols)
+    dm = P.DeviceModel.from_model(m, scale_dtype="f16")
+    for B in (1, 5, 16):
+        ps = [2 + (b * 7 + B) % 3 for b in range(B)]
+        X = np.stack([O.random_gaussian(1, cols, seed=100 + b).ravel() for b in range(B)])
+        Xh = X.astype(np.float16).astype(np.float32)  # the kernel computes on fp16 x
+        Y = dm.gemm_mixedp(ps, torch.from_numpy(Xh).cuda()).cpu().numpy()
+        for b, p in enumerate(ps):
+            a16 = m.scale_sets[p].alpha.astype(np.float16).astype(np.float32)
+            z = m.scale_sets[p].offset
+            z16 = None if z is None else z.astype(np.float16).astype(np.float32)
+            want = O.gemv_lut(m.bitplanes.words, cols, 128, a16, z16, p, Xh[b])
+            assert O.rel_dev(Y[b], want) <= 1e-4, (B, b, p, O.rel_dev(Y[b], want))

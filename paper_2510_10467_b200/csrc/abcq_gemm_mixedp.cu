@@ -29,6 +29,16 @@ namespace abcq {
 
 constexpr int kGWarps = 8;
 constexpr int kMaxBatch = 16;
+constexpr int kMaxStagePlanes = 4;  // planes staged per item (p_max > 4 loads the rest in rounds)
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 struct GemmArgs {
     const uint4* planes;
@@ -53,6 +63,9 @@ template <typename ST, bool ASYM>
 __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArgs a) {
     __shared__ __align__(16) uint2 nib_tab[16];                    // nibble -> {half2, half2}
     __shared__ __align__(16) unsigned char scratch[kGWarps][512];  // per-warp un-rotated block
+    // per-warp double buffer of an item's plane blocks, filled with cp.async
+    // (group-tracked, so the next item streams in while this one computes)
+    __shared__ __align__(16) uint4 stage[kGWarps][2][kMaxStagePlanes][32];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 16) {
@@ -109,14 +122,34 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
     const int preq0 = g < B ? a.p_of[g] : 0, preq1 = g + 8 < B ? a.p_of[g + 8] : 0;
     const int64_t pstride = (int64_t)B * a.NRT * kTileRows;
 
-    for (int rt = widx; rt < a.NRT; rt += wps) {
+    // issue the cp.async copies of item rt's planes [i0, i0 + n) into buffer bf
+    auto stage_item = [&](int rt, int bf, int i0) {
+        if (rt < a.NRT) {
+            const int item = s * a.NRT + rt;
+            for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i)
+                cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
+        }
+        cp_async_commit();
+    };
+    int buf = 0;
+    stage_item(widx, 0, 0);
+    for (int rt = widx; rt < a.NRT; rt += wps, buf ^= 1) {
         const int item = s * a.NRT + rt;
         // accumulators: requests {g, g+8} x tile rows {2t, 2t+1, 8+2t, 8+2t+1}
         float y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         for (int i = 0; i < a.pmax; ++i) {
+            if (i % kMaxStagePlanes == 0) {
+                // planes [i, i+4) of this item are (being) staged in `buf`: prefetch the
+                // next round (more planes of this item, or the next item) into buf^1
+                if (i + kMaxStagePlanes < a.pmax) stage_item(rt, buf ^ 1, i + kMaxStagePlanes);
+                else stage_item(rt + wps, buf ^ 1, 0);
+                cp_async_wait<1>();
+                __syncwarp();
+            }
             // un-rotate this plane's 512-byte block into logical row-major bytes:
             // lane (half, r) holds group (2s + half) bytes of row r rotated by r
-            const uint4 blk = __ldg(a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
+            const uint4 blk = stage[warp][buf][i % kMaxStagePlanes][lane];
+            if (i % kMaxStagePlanes == kMaxStagePlanes - 1 && i + 1 < a.pmax) buf ^= 1;  // next round staged in buf^1
             {
                 const int half = lane >> 4, r = lane & 15;
                 const uint32_t wv[4] = {blk.x, blk.y, blk.z, blk.w};

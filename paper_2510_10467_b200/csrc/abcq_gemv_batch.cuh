@@ -34,7 +34,10 @@ struct Job {
     void* y;
     float* partial;      // [NS][NRT*16]
     uint32_t* counters;  // [NRT] arrival counters, self-resetting
-    int rows, cols, NRT, NS, p, items, q, rem;
+    int rows, cols, NRT, NS, p, items;
+    int ibase;      // first item of this job in the batch's item sequence
+    int w;          // cost units per item: p blocks + the item's share of a table build
+    int64_t ubase;  // first cost unit of this job (sum of items * w before it)
 };
 
 // kernel parameter: NJ job slots (1, 4 or 16 -- the smallest that fits)
@@ -42,6 +45,8 @@ template <int NJ>
 struct KArgs {
     Job jobs[NJ];
     int n_jobs;
+    int total_items;
+    int64_t total_units;
     int fused;
     int dbg;  // profiling experiments: 1 = skip the lookups
     unsigned long long* trace;
@@ -50,6 +55,8 @@ struct KArgs {
 struct BatchArgs {
     Job jobs[kMaxJobs];
     int n_jobs;
+    int total_items;
+    int64_t total_units;
     int fused;  // 1: in-kernel split-K completion; 0: split_reduce_kernel follows
     int dbg;
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
@@ -70,29 +77,81 @@ struct SlotGeom {
         (int)(2 * kTableWindow - 0x400) + (kWarps * kRing > kLow ? kWarps * kRing - kLow : 0) * kBytes;
 };
 
-// This warp's items of job J in CTA b: the CTA's range [it0, it1) has <= 2
-// segments (slices); warps split proportionally to the segment sizes, then
-// each warp gets a contiguous run.
-struct WarpRun {
-    int lo, hi, seg, s0;  // items [lo, hi) of slice s0 + seg
-    __device__ __forceinline__ int n() const { return hi - lo; }
+// ---------------------------------------------------------------------------
+// Work schedule. The batch's items (job-major, then slice-major as stored) form
+// one sequence; an item of job j costs w_j units: its p_j 512-byte blocks plus
+// its share of a piece's fixed cost (table build, barrier: ~kPieceBlocks
+// blocks' worth, spread over the NRT items of a slice), so CTAs that cross
+// many small slices get fewer bytes. CTA b owns the items whose first cost
+// unit lies in [b*U/G, (b+1)*U/G). A CTA's range is cut into "rounds" of at
+// most two pieces, a piece being the range's items of one (job, slice): one
+// lookup-table build (two 32-column table segments) and one CTA barrier per
+// round. Within a round the warps split the cost evenly; a warp's run may
+// cover the tail of piece 0 and the head of piece 1 (two sub-runs).
+// ---------------------------------------------------------------------------
+struct Piece {
+    int j, s, lo, hi;  // job, slice, batch items [lo, hi)
 };
-__device__ __forceinline__ WarpRun warp_run(const Job& J, int b, int warp) {
-    WarpRun r;
-    const int it0 = b * J.q + min(b, J.rem);
-    const int it1 = it0 + J.q + (b < J.rem ? 1 : 0);
-    r.s0 = J.NRT > 0 ? it0 / J.NRT : 0;
-    const int split = min((r.s0 + 1) * J.NRT, it1);
-    const int n0 = split - it0, n1 = it1 - split, n = it1 - it0;
-    int w0 = n1 == 0 ? kWarps : (n0 == 0 ? 0 : (kWarps * n0 + n / 2) / max(n, 1));
-    if (n0 > 0 && w0 == 0) w0 = 1;
-    if (n1 > 0 && w0 == kWarps) w0 = kWarps - 1;
-    r.seg = warp < w0 ? 0 : 1;
-    const int nw = r.seg ? kWarps - w0 : w0, wi = r.seg ? warp - w0 : warp;
-    const int base = r.seg ? split : it0, cnt = r.seg ? n1 : n0;
-    r.lo = base + (int)((int64_t)wi * cnt / max(nw, 1));
-    r.hi = base + (int)((int64_t)(wi + 1) * cnt / max(nw, 1));
-    return r;
+struct Round {
+    Piece pc[2];
+    int nseg, end;  // pc[1] valid iff nseg == 2; end = pc[nseg-1].hi
+};
+struct WarpRun {
+    int lo, hi;  // batch items; sub-run k = [lo, hi) intersected with piece k
+};
+
+template <int NJ>
+__device__ __forceinline__ int first_item(const KArgs<NJ>& a, int64_t u) {
+    int j = 0;
+    while (j + 1 < a.n_jobs && a.jobs[j + 1].ubase <= u) ++j;
+    const Job& J = a.jobs[j];
+    const int64_t loc = (u - J.ubase + J.w - 1) / J.w;
+    return J.ibase + (int)(loc < J.items ? loc : J.items);
+}
+template <int NJ>
+__device__ __forceinline__ Piece piece_at(const KArgs<NJ>& a, int g, int it1) {
+    Piece P;
+    P.j = 0;
+    while (P.j + 1 < a.n_jobs && a.jobs[P.j + 1].ibase <= g) ++P.j;
+    const Job& J = a.jobs[P.j];
+    P.s = (g - J.ibase) / J.NRT;
+    P.lo = g;
+    P.hi = min(J.ibase + (P.s + 1) * J.NRT, it1);
+    return P;
+}
+template <int NJ>
+__device__ __forceinline__ Round make_round(const KArgs<NJ>& a, int g, int it1) {
+    Round R;
+    R.pc[0] = piece_at(a, g, it1);
+    R.pc[1] = R.pc[0];
+    R.nseg = 1;
+    R.end = R.pc[0].hi;
+    if (R.end < it1) {
+        R.pc[1] = piece_at(a, R.end, it1);
+        R.nseg = 2;
+        R.end = R.pc[1].hi;
+    }
+    return R;
+}
+template <int NJ>
+__device__ __forceinline__ WarpRun warp_run(const KArgs<NJ>& a, const Round& R, int warp) {
+    const int p0 = a.jobs[R.pc[0].j].p, p1 = a.jobs[R.pc[1].j].p;
+    const int64_t c0 = (int64_t)(R.pc[0].hi - R.pc[0].lo) * p0;
+    const int64_t c = c0 + (R.nseg == 2 ? (int64_t)(R.pc[1].hi - R.pc[1].lo) * p1 : 0);
+    auto item_at = [&](int64_t pos) -> int {  // first item starting at or after cost pos
+        if (pos <= c0) return R.pc[0].lo + (int)((pos + p0 - 1) / p0);
+        return R.pc[1].lo + (int)((pos - c0 + p1 - 1) / p1);
+    };
+    WarpRun w;
+    w.lo = item_at(warp * c / kWarps);
+    w.hi = item_at((warp + 1) * c / kWarps);
+    return w;
+}
+__device__ __forceinline__ int sub_lo(const WarpRun& w, const Round& R, int k) {
+    return k == 0 ? w.lo : max(w.lo, R.pc[0].hi);
+}
+__device__ __forceinline__ int sub_hi(const WarpRun& w, const Round& R, int k) {
+    return k == 0 ? min(w.hi, R.pc[0].hi) : (R.nseg == 2 ? w.hi : w.lo);
 }
 
 // fixed-order sum of one row's NS slice partials (4 interleaved chains over
@@ -110,9 +169,32 @@ __device__ __forceinline__ float reduce_row(const float* pp, int NS, int64_t str
     return (c[0] + c[1]) + (c[2] + c[3]);
 }
 
-#define ABCQ_BTRACE(k)                                                           \
-    do {                                                                         \
-        if (a.trace && lane == 0) a.trace[blockIdx.x * 8 + (k)] = globaltimer(); \
+// 16 entries of chunk c of the lookup table, t = u + 16*h (h = 0..15), from the
+// chunk's 8 x values: the shared prefix over x0..x3 (bits of u) once, then the
+// binary tree over x4..x7 -- every entry keeps the reference's f32 rounding
+// sequence ((((0 -/+ x0) -/+ x1) ...) -/+ x7) (gemv.py:67-81), 34 adds
+__device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, float (&leaf)[16]) {
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v = ((u >> j) & 1) ? v + xs[j] : v - xs[j];
+    leaf[0] = v;
+#pragma unroll
+    for (int j = 4; j < 8; ++j) {
+        const int n = 1 << (j - 4);  // leaves so far: index = bits 4..j-1 of t
+#pragma unroll
+        for (int k = n - 1; k >= 0; --k) {
+            leaf[k + n] = leaf[k] + xs[j];
+            leaf[k] = leaf[k] - xs[j];
+        }
+    }
+}
+
+// profiling stamps (abcq_debug_set_trace): per CTA, slot k = max over the
+// calling warps of %globaltimer. 0 start, 1 after the PDL wait, 2 first table
+// ready, 3 streams done, 4 arrivals published, 5 split-K completed, 6 = rounds
+#define ABCQ_BTRACE(k)                                                                   \
+    do {                                                                                 \
+        if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
     } while (0)
 
 template <int NJ, typename XT, typename YT, typename ST, bool ASYM>
@@ -141,54 +223,75 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         fence_mbar_init();
     }
     __syncwarp();
+    const int it0 = first_item(a, (int64_t)b * a.total_units / G);
+    const int it1 = first_item(a, (int64_t)(b + 1) * a.total_units / G);
 
-    // ---- this warp's slot stream: over jobs j, chunks of kK items, planes i --
-    // issue cursor: element (job j, chunk start c, plane i) with its source
-    // pointers kept in registers and advanced incrementally (the job table in
-    // parameter space is only read when the cursor enters a new job)
+    // ---- this warp's slot stream: rounds -> sub-runs -> chunks of kK items ->
+    // planes; the issue cursor keeps its source pointers in registers and
+    // advances them incrementally (the job table in parameter space is read
+    // only when the cursor enters a new sub-run)
     struct Cur {
-        int j, hi, c, i, p;
-        const char* w;   // planes + i*plane_stride + c*512   (bytes)
-        const ST* al;    // alpha + (i*items + c)*32
-        const ST* z;     // offset + c*32
-        int64_t pst;     // plane stride (bytes)
-        int64_t ast;     // items*32: scale elements per plane
+        int rs, rend, mid, whi;  // round start / end, piece boundary, warp run end
+        int hi, c, i, p;         // sub-run end, chunk start, plane, job precision
+        const char* w;           // planes + i*plane_stride + item*512   (bytes)
+        const ST* al;            // alpha + (i*items + item)*32
+        const ST* z;             // offset + item*32
+        int64_t pst;             // plane stride (bytes)
+        int64_t ast;             // items*32: scale elements per plane
     };
-    auto cur_job = [&](Cur& k, int j) {
-        for (; j < a.n_jobs; ++j) {
-            const Job& J = a.jobs[j];
-            const WarpRun r = warp_run(J, b, warp);
-            if (r.n() > 0) {
-                k.j = j;
-                k.hi = r.hi;
-                k.c = r.lo;
-                k.i = 0;
-                k.p = J.p;
-                k.pst = J.plane_stride_u4 * 16;
-                k.ast = (int64_t)J.items * 32;
-                k.w = reinterpret_cast<const char*>(J.planes) + (int64_t)r.lo * kBlockBytes;
-                k.al = static_cast<const ST*>(J.alpha) + (int64_t)r.lo * 32;
-                k.z = ASYM ? static_cast<const ST*>(J.offset) + (int64_t)r.lo * 32 : nullptr;
+    auto enter_sub = [&](Cur& k, int j, int lo, int hi) {
+        const Job& J = a.jobs[j];
+        const int loc = lo - J.ibase;
+        k.hi = hi;
+        k.c = lo;
+        k.i = 0;
+        k.p = J.p;
+        k.pst = J.plane_stride_u4 * 16;
+        k.ast = (int64_t)J.items * 32;
+        k.w = reinterpret_cast<const char*>(J.planes) + (int64_t)loc * kBlockBytes;
+        k.al = static_cast<const ST*>(J.alpha) + (int64_t)loc * 32;
+        k.z = ASYM ? static_cast<const ST*>(J.offset) + (int64_t)loc * 32 : nullptr;
+    };
+    // first non-empty sub-run at or after round start rs (k.rs = it1: exhausted)
+    auto enter_round = [&](Cur& k, int rs) {
+        for (; rs < it1;) {
+            const Round Rn = make_round(a, rs, it1);
+            const WarpRun wr = warp_run(a, Rn, warp);
+            k.rs = rs;
+            k.rend = Rn.end;
+            k.mid = Rn.pc[0].hi;
+            k.whi = sub_hi(wr, Rn, 1);
+            const int lo0 = sub_lo(wr, Rn, 0), hi0 = sub_hi(wr, Rn, 0);
+            const int lo1 = sub_lo(wr, Rn, 1), hi1 = sub_hi(wr, Rn, 1);
+            const bool first = lo0 < hi0;
+            if (first || lo1 < hi1) {  // (selects, not an indexed Round: no local memory)
+                enter_sub(k, first ? Rn.pc[0].j : Rn.pc[1].j, first ? lo0 : lo1, first ? hi0 : hi1);
                 return;
             }
+            rs = Rn.end;
         }
-        k.j = a.n_jobs;  // exhausted
+        k.rs = it1;
     };
     auto advance = [&](Cur& k) {
         if (++k.i < k.p) {
             k.w += k.pst;
             k.al += k.ast;
-        } else {
-            k.i = 0;
-            k.c += kK;
-            if (k.c >= k.hi) {
-                cur_job(k, k.j + 1);
-            } else {
-                k.w += kK * kBlockBytes - (k.p - 1) * k.pst;
-                k.al += kK * 32 - (k.p - 1) * k.ast;
-                if constexpr (ASYM) k.z += kK * 32;
-            }
+            return;
         }
+        k.i = 0;
+        k.c += kK;
+        if (k.c < k.hi) {
+            k.w += kK * kBlockBytes - (k.p - 1) * k.pst;
+            k.al += kK * 32 - (k.p - 1) * k.ast;
+            if constexpr (ASYM) k.z += kK * 32;
+            return;
+        }
+        if (k.hi == k.mid && k.whi > k.mid) {  // sub-run 0 done, sub-run 1 follows
+            const Round Rn = make_round(a, k.rs, it1);
+            enter_sub(k, Rn.pc[1].j, k.mid, k.whi);
+            return;
+        }
+        enter_round(k, k.rend);
     };
     // issue the TMA copies of the cursor's element into slot s (lane 0 only)
     auto issue = [&](const Cur& k, int s) {
@@ -205,13 +308,14 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     };
 
     Cur ic;  // issue cursor: runs R elements ahead of consumption
-    cur_job(ic, 0);
+    enter_round(ic, it0);
     // static model data: fill the ring before waiting on the previous kernel
-    for (int s = 0; s < R && ic.j < a.n_jobs; ++s) {
+    for (int s = 0; s < R && ic.rs < it1; ++s) {
         issue(ic, s);
         advance(ic);
     }
     pdl_wait();  // x, y and the workspace belong to the previous kernel
+    if (warp == 0) ABCQ_BTRACE(1);
     pdl_launch_dependents();
 
     const int half = lane >> 4, r = lane & 15;
@@ -227,73 +331,67 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         rb[k] = v | ((kTableWindow >> 16) << 24);  // byte 3 -> address byte 2
     }
 
-    // x values of this thread's table tasks (chunk tid&31 of up to 2 slices)
-    static_assert(kBThreads == 512, "table build maps one thread to (chunk, hi) of a slice");
+    // x values of this thread's table tasks: chunk tid&31 of the round's pieces
+    static_assert(kBThreads == 512, "table build maps one thread to (chunk, u) of a slice");
     float xpre[2][8];
-    int xpre_job = -1;
-    auto prefetch_x = [&](int jn) {
-        const Job& Jn = a.jobs[jn];
-        const int it0 = b * Jn.q + min(b, Jn.rem);
-        const int sn = Jn.NRT > 0 ? it0 / Jn.NRT : 0;
-        const XT* __restrict__ xn = static_cast<const XT*>(Jn.x);
+    auto prefetch_x = [&](const Round& Rn) {
 #pragma unroll
-        for (int ts = 0; ts < 2; ++ts)  // slice sn + 1 may not exist: load_x8 zero-fills past cols
-            load_x8<XT>(xn, (sn + ts) * kSliceCols + 8 * (tid & 31), Jn.cols, xpre[ts]);
-        xpre_job = jn;
+        for (int ts = 0; ts < 2; ++ts) {
+            if (ts < Rn.nseg) {
+                const Job& Jn = a.jobs[Rn.pc[ts].j];
+                load_x8<XT>(static_cast<const XT*>(Jn.x), Rn.pc[ts].s * kSliceCols + 8 * (tid & 31), Jn.cols,
+                            xpre[ts]);
+            }
+        }
     };
 
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
-    for (int j = 0; j < a.n_jobs; ++j) {
-        const Job& J = a.jobs[j];
-        const int it0 = b * J.q + min(b, J.rem), it1 = it0 + J.q + (b < J.rem ? 1 : 0);
-        if (it1 <= it0) continue;  // no items for this CTA: nothing to build or stream
-        const WarpRun wr = warp_run(J, b, warp);
-        const int s0 = wr.s0;
-        const int nseg = it1 > min((s0 + 1) * J.NRT, it1) ? 2 : 1;
-        // ---- lookup tables of job j's slices (one CTA barrier each side) ------
-        // thread (c, hi) of task ts builds 16 entries of chunk c from 8 x values;
-        // they were prefetched into registers while the previous job streamed
-        if (xpre_job != j) prefetch_x(j);
-        if (j > 0) __syncthreads();  // every warp is done with the previous table
+    int round = 0;
+    if (it0 < it1) prefetch_x(make_round(a, it0, it1));
+    for (int rs = it0; rs < it1; ++round) {
+        const Round Rd = make_round(a, rs, it1);
+        // ---- lookup tables of the round's pieces (one CTA barrier each side) ---
+        // thread (c, u) builds the 16 entries t = u + 16h of chunk c from 8 x
+        // values, prefetched into registers while the previous round streamed
+        if (round > 0) __syncthreads();  // every warp is done with the previous table
 #pragma unroll
         for (int ts = 0; ts < 2; ++ts) {
-            if (ts < nseg) {
-                const int c = tid & 31, hi = tid >> 5;
+            if (ts < Rd.nseg) {
+                const int c = tid & 31, u = tid >> 5;
                 float ev[16];
-                lut_chunk_entries16(xpre[ts], hi, ev);
+                lut_chunk_column16(xpre[ts], u, ev);
                 float* col = table + ts * 32 + c;
 #pragma unroll
-                for (int t = 0; t < 16; ++t) col[(hi * 16 + t) * 64] = ev[t];
-                if (ASYM && hi == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
+                for (int h = 0; h < 16; ++h) col[(u + 16 * h) * 64] = ev[h];
+                if (ASYM && u == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
             }
         }
         __syncthreads();
-        for (int jn = j + 1; jn < a.n_jobs; ++jn) {  // x of the next job this CTA works on
-            const Job& Jn = a.jobs[jn];
-            if (Jn.q + (b < Jn.rem ? 1 : 0) > 0) {
-                prefetch_x(jn);
-                break;
-            }
-        }
-        if (j < 3 && warp == 0) ABCQ_BTRACE(1 + 2 * j);
-        if (wr.n() == 0) continue;
-        float gx = 0.f;
-        if constexpr (ASYM) {
-            for (int c = 0; c < 16; ++c) gx += csum[wr.seg * 32 + half * 16 + c];
-        }
+        if (Rd.end < it1) prefetch_x(make_round(a, Rd.end, it1));
+        if (round == 0 && warp == 0) ABCQ_BTRACE(2);
+        const WarpRun wr = warp_run(a, Rd, warp);
 
-        // ---- stream this warp's elements of job j -------------------------------
-        YT* __restrict__ y = static_cast<YT*>(J.y);
-        const int64_t pstride = (int64_t)J.NRT * kTileRows;
-        const int sl = s0 + wr.seg;
+        // ---- stream this warp's elements of the round ---------------------------
         auto run = [&](auto seg_tag) {
             constexpr int SEG = decltype(seg_tag)::value;
-            for (int c = wr.lo; c < wr.hi; c += kK) {
-                const int cnt = min(kK, wr.hi - c);
+            const int lo = sub_lo(wr, Rd, SEG), hi = sub_hi(wr, Rd, SEG);
+            if (lo >= hi) return;
+            const Piece& P = Rd.pc[SEG];
+            const Job& J = a.jobs[P.j];
+            float gx = 0.f;
+            if constexpr (ASYM) {
+                for (int c = 0; c < 16; ++c) gx += csum[SEG * 32 + half * 16 + c];
+            }
+            YT* __restrict__ y = static_cast<YT*>(J.y);
+            float* __restrict__ part = J.partial + (int64_t)P.s * J.NRT * kTileRows;
+            const int tile0 = J.ibase + P.s * J.NRT;  // batch item of row tile 0 of this slice
+            const int p = J.p, NS = J.NS, rows = J.rows;
+            for (int c = lo; c < hi; c += kK) {
+                const int cnt = min(kK, hi - c);
                 float acc[kK];
 #pragma unroll
                 for (int q = 0; q < kK; ++q) acc[q] = 0.f;
-                for (int i = 0; i < J.p; ++i, ++e) {
+                for (int i = 0; i < p; ++i, ++e) {
                     const int s = e % R;
                     mbar_wait(&mybar[s], (e / R) & 1);
                     const char* st = slot_ptr(warp * R + s);
@@ -330,95 +428,129 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                         }
                     }
                     __syncwarp();  // every lane has consumed slot s
-                    if (ic.j < a.n_jobs) {  // refill it with the element R ahead
+                    if (ic.rs < it1) {  // refill it with the element R ahead
                         issue(ic, s);
                         advance(ic);
                     }
                 }
                 // chunk done: combine the slice's two groups (lanes l, l+16), emit 16 rows per item
+                float outv[kK];
 #pragma unroll
-                for (int q = 0; q < kK; ++q) {
-                    const float out = acc[q] + __shfl_down_sync(0xffffffffu, acc[q], 16);
-                    if (q < cnt && lane < 16) {
-                        const int row = (c + q - sl * J.NRT) * kTileRows + lane;
-                        if (J.NS == 1) {
-                            if (row < J.rows) y[row] = from_f32<YT>(out);
-                        } else {
-                            __stcg(J.partial + sl * pstride + row, out);
-                        }
+                for (int q = 0; q < kK; ++q) outv[q] = acc[q] + __shfl_down_sync(0xffffffffu, acc[q], 16);
+                if (NS == 1) {
+#pragma unroll
+                    for (int q = 0; q < kK; ++q) {
+                        const int row = (c + q - tile0) * kTileRows + lane;
+                        if (q < cnt && lane < 16 && row < rows) y[row] = from_f32<YT>(outv[q]);
                     }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < kK; ++q)
+                        if (q < cnt && lane < 16) __stcg(part + (c + q - tile0) * kTileRows + lane, outv[q]);
                 }
             }
         };
-        if (wr.seg)
-            run(std::integral_constant<int, 1>{});
-        else
-            run(std::integral_constant<int, 0>{});
-        if (j < 3 && warp == 0) ABCQ_BTRACE(2 + 2 * j);
+        run(std::integral_constant<int, 0>{});
+        run(std::integral_constant<int, 1>{});
+        rs = Rd.end;
     }
 
+    ABCQ_BTRACE(3);
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 6] = round;
     if (!a.fused) return;
-    // ---- split-K completion of every job (NS > 1), after all streams --------
-    // 1. publish: one fence per warp, then per-row-tile arrival counters
+    // ---- split-K completion of every job with NS > 1 -------------------------
+    // 1. publish: one fence per warp, then one arrival per streamed item on its
+    //    row tile's counter
     __syncwarp();
-    if (lane == 0) __threadfence();
-    __syncwarp();
+    __threadfence();
+    for (int rs = it0; rs < it1;) {
+        const Round Rd = make_round(a, rs, it1);
+        const WarpRun wr = warp_run(a, Rd, warp);
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb) {
+            const Job& J = a.jobs[Rd.pc[sb].j];
+            if (sb >= Rd.nseg || J.NS <= 1) continue;
+            const int tile0 = J.ibase + Rd.pc[sb].s * J.NRT;
+            for (int it = sub_lo(wr, Rd, sb) + lane; it < sub_hi(wr, Rd, sb); it += 32)
+                atomicAdd(&J.counters[it - tile0], 1u);
+        }
+        rs = Rd.end;
+    }
+    ABCQ_BTRACE(4);
+    // 2. CTA b completes row tiles [b*NRT/G, (b+1)*NRT/G) of every split job:
+    //    warp w takes the CTA's tiles w, w+16, ... (flattened over jobs); per
+    //    tile all lanes wait for the NS arrivals, then lane (r, h) sums row r's
+    //    chains 2h, 2h+1 -- reduce_row's fixed order, so the result is bitwise
+    //    equal to split_reduce_kernel -- and the tile's counter is reset (this
+    //    CTA is its only reader).
+    int ntiles = 0;
     for (int j = 0; j < a.n_jobs; ++j) {
         const Job& J = a.jobs[j];
-        if (J.NS <= 1) continue;
-        const WarpRun wr = warp_run(J, b, warp);
-        for (int it = wr.lo + lane; it < wr.hi; it += 32) atomicAdd(&J.counters[it - (wr.s0 + wr.seg) * J.NRT], 1u);
+        if (J.NS > 1) ntiles += (int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G);
     }
-    // 2. this CTA reduces an even share of every job's row tiles once all NS
-    //    slices arrived; (job, row) pairs of all jobs are spread over the
-    //    threads so the batch pays ONE latency round, not one per job
-    //    (thread per row, reduce_row order -> bitwise equal to the unfused path)
-    {
-        int total = 0;
-        for (int j = 0; j < a.n_jobs; ++j) {
+    const int hh = lane >> 4;
+    for (int f = warp; f < ntiles; f += kWarps) {
+        int j = 0, lt = f;
+        for (;; ++j) {  // job j, local tile lt of flat tile index f
             const Job& J = a.jobs[j];
-            if (J.NS > 1) total += ((int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G)) * kTileRows;
+            if (J.NS <= 1) continue;
+            const int n = (int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G);
+            if (lt < n) break;
+            lt -= n;
         }
-        for (int f = tid; f < total; f += kBThreads) {
-            int j = 0, lr = f;
-            for (;; ++j) {  // locate job j and local row lr of flat index f
-                const Job& J = a.jobs[j];
-                if (J.NS <= 1) continue;
-                const int n = ((int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G)) * kTileRows;
-                if (lr < n) break;
-                lr -= n;
+        const Job& J = a.jobs[j];
+        const int rt = (int)((int64_t)b * J.NRT / G) + lt;
+        uint32_t seen;
+        for (int backoff = 64;;) {  // poll gently: spinning warps steal L2 slots from the streams
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.counters + rt) : "memory");
+            if (seen >= (uint32_t)J.NS) break;
+            __nanosleep(backoff);
+            backoff = min(backoff * 2, 1024);
+        }
+        const int row = rt * kTileRows + (lane & 15);
+        const int64_t stride = (int64_t)J.NRT * kTileRows;
+        const float* pp = J.partial + row;
+        float c2[2] = {0.f, 0.f};
+        for (int s0 = 0; s0 < J.NS; s0 += 16) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // terms s0 + 4m + 2h + {0,1} of chains 2h, 2h+1
+                const int sl = s0 + (k >> 1) * 4 + 2 * hh + (k & 1);
+                v[k] = sl < J.NS ? __ldcg(pp + sl * stride) : 0.f;
             }
-            const Job& J = a.jobs[j];
-            const int rt_lo = (int)((int64_t)b * J.NRT / G);
-            const int rt = rt_lo + lr / kTileRows;
-            const uint32_t* cptr = J.counters + rt;
-            uint32_t seen;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cptr) : "memory");
-            } while (seen < (uint32_t)J.NS);
-            const int row = rt_lo * kTileRows + lr;
-            const float v = reduce_row(J.partial + row, J.NS, (int64_t)J.NRT * kTileRows);
-            if (row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) c2[k & 1] += v[k];
         }
+        const float mine = c2[0] + c2[1];
+        const float other = __shfl_down_sync(0xffffffffu, mine, 16);
+        if (lane < 16 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
+        if (lane == 0) J.counters[rt] = 0u;  // self-reset for the next launch
     }
-    __syncthreads();  // every counter of this CTA's share was consumed
-    for (int j = 0; j < a.n_jobs; ++j) {
-        const Job& J = a.jobs[j];
-        if (J.NS <= 1) continue;
-        const int rt_lo = (int)((int64_t)b * J.NRT / G), rt_hi = (int)((int64_t)(b + 1) * J.NRT / G);
-        for (int rt = rt_lo + tid; rt < rt_hi; rt += kBThreads) J.counters[rt] = 0u;  // self-reset
-    }
-    if (warp == 0) ABCQ_BTRACE(7);
+    ABCQ_BTRACE(5);
 }
 
-// Split-K completion as a separate PDL-chained kernel (single GEMVs)
-template <typename YT>
-__global__ void __launch_bounds__(64) split_reduce_kernel(const float* __restrict__ partial, int NS,
-                                                          int64_t stride, int rows, YT* __restrict__ y) {
+// Split-K completion as ONE PDL-chained kernel for the whole batch: block k
+// sums kReduceRows rows of one split job (blocks are laid out job by job, so
+// the job lookup is block-uniform); reduce_row's fixed order, so the result is
+// bitwise equal to the in-kernel completion (debug mode 21).
+constexpr int kReduceRows = 128;
+template <int NJ, typename YT>
+__global__ void __launch_bounds__(kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
     pdl_wait();
     pdl_launch_dependents();
-    const int row = blockIdx.x * blockDim.x + threadIdx.x;
-    if (row < rows) y[row] = from_f32<YT>(reduce_row(partial + row, NS, stride));
+    int blk = blockIdx.x, j = 0;
+    for (; j < a.n_jobs; ++j) {
+        const Job& J = a.jobs[j];
+        if (J.NS <= 1) continue;
+        const int nb = (J.rows + kReduceRows - 1) / kReduceRows;
+        if (blk < nb) break;
+        blk -= nb;
+    }
+    if (j >= a.n_jobs) return;
+    const Job& J = a.jobs[j];
+    const int row = blk * kReduceRows + threadIdx.x;
+    if (row < J.rows)
+        static_cast<YT*>(J.y)[row] = from_f32<YT>(reduce_row(J.partial + row, J.NS, (int64_t)J.NRT * kTileRows));
 }
 
 template <int NJ, typename XT, typename YT, typename ST, bool ASYM>
@@ -426,6 +558,8 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     KArgs<NJ> a;
     for (int j = 0; j < ba.n_jobs; ++j) a.jobs[j] = ba.jobs[j];
     a.n_jobs = ba.n_jobs;
+    a.total_items = ba.total_items;
+    a.total_units = ba.total_units;
     a.fused = ba.fused;
     a.dbg = ba.dbg;
     a.trace = ba.trace;
@@ -453,18 +587,15 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess || a.fused) return (int)e;
-    for (int j = 0; j < a.n_jobs; ++j) {  // unfused: one reduce kernel per split job
-        const Job& J = a.jobs[j];
-        if (J.NS <= 1) continue;
-        cudaLaunchConfig_t rc = cfg;
-        rc.blockDim = dim3(64);
-        rc.gridDim = dim3((unsigned)ceil_div(J.rows, 64));
-        rc.dynamicSmemBytes = 0;
-        e = cudaLaunchKernelEx(&rc, split_reduce_kernel<YT>, (const float*)J.partial, J.NS,
-                               (int64_t)J.NRT * kTileRows, J.rows, static_cast<YT*>(J.y));
-        if (e != cudaSuccess) return (int)e;
-    }
-    return 0;
+    int nblocks = 0;  // one reduce launch for every split job of the batch
+    for (int j = 0; j < a.n_jobs; ++j)
+        if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
+    if (nblocks == 0) return 0;
+    cudaLaunchConfig_t rc = cfg;
+    rc.blockDim = dim3(kReduceRows);
+    rc.gridDim = dim3((unsigned)nblocks);
+    rc.dynamicSmemBytes = 0;
+    return (int)cudaLaunchKernelEx(&rc, batch_reduce_kernel<NJ, YT>, a);
 }
 
 template <typename XT, typename YT, typename ST, bool ASYM>

@@ -7,6 +7,10 @@ namespace abcq {
 
 unsigned long long* g_trace = nullptr;  // abcq_debug_set_trace (profiling aid)
 int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experiments)
+// fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
+// abcq_debug_set_mode(1000 + v) sets it to v)
+int g_piece_blocks = 150;
+constexpr int kCostScale = 64;
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
@@ -23,15 +27,13 @@ bool lut_supports(const abcq_model_t* m, int p) {
 int lut_max_jobs() { return kMaxJobs; }
 
 // fill a Job from a model + call; ws points at this job's workspace region
-static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* y, char* ws, int grid) {
+static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* y, char* ws) {
     J.rows = m->rows;
     J.cols = m->cols;
     J.NRT = n_row_tiles(m->rows);
     J.NS = n_slices(m->cols);
     J.p = p;
     J.items = J.NRT * J.NS;
-    J.q = J.items / grid;
-    J.rem = J.items % grid;
     J.planes = static_cast<const uint4*>(m->planes);
     J.plane_stride_u4 = m->plane_stride_bytes / 16;
     J.alpha = m->alpha[p];
@@ -55,14 +57,24 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms();
     char* w = static_cast<char*>(ws);
+    int items = 0;
+    int64_t units = 0;
     for (int j = 0; j < n; ++j) {
-        make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w, grid);
+        make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
         w += lut_workspace_bytes(models[j]);
+        Job& J = a.jobs[j];
+        J.ibase = items;
+        J.ubase = units;
+        J.w = kCostScale * ps[j] + (int)ceil_div((int64_t)kCostScale * g_piece_blocks, J.NRT);
+        items += J.items;
+        units += (int64_t)J.items * J.w;
     }
     a.n_jobs = n;
-    // a batch pays the split-K tail once, in-kernel; a single GEMV hands it to
-    // a PDL-chained reduce kernel (shorter critical path, measured)
-    a.fused = (n > 1 && g_dbg_mode != 20) || g_dbg_mode == 21;
+    a.total_items = items;
+    a.total_units = units;
+    // split-K completion: one PDL-chained batch_reduce_kernel; debug mode 21
+    // completes in-kernel instead (arrival counters + polling sweep)
+    a.fused = g_dbg_mode == 21;
     a.dbg = g_dbg_mode == 1 ? 1 : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;

@@ -280,6 +280,26 @@ def test_gemv_batch_matches_single_calls(P):
         assert torch.equal(out, w)
 
 
+@pytest.mark.parametrize("rows,cols", [(4096, 4096), (4096, 14336), (300, 1024)])
+def test_split_completion_paths_bitwise(P, rows, cols):
+    """In-kernel last-arriver split-K completion (default) == the separate
+    in-kernel completion (debug mode 21), bitwise, repeatedly (the
+    arrival counters self-reset)."""
+    from paper_2510_10467_b200 import _lib
+    dm = P.DeviceModel.from_model(synth_model(P, rows, cols, 2, 4, seed=rows ^ cols), scale_dtype="f16")
+    x = torch.from_numpy(O.random_gaussian(1, cols, seed=5).ravel()).cuda().half()
+    for p in (2, 3, 4):
+        fused = [dm.gemv(p, x).clone() for _ in range(3)]
+        _lib.lib().abcq_debug_set_mode(21)
+        try:
+            unfused = dm.gemv(p, x).clone()
+        finally:
+            _lib.lib().abcq_debug_set_mode(0)
+        torch.cuda.synchronize()
+        for f in fused:
+            assert torch.equal(f, unfused), p
+
+
 def test_gemv_batch_asymmetric(P):
     from paper_2510_10467_b200.device_model import gemv_batch
     ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]

@@ -94,7 +94,7 @@ if "ABCQ_TRACE" in __import__("os").environ:
     t = buf.view(16, 160, 8).cpu().numpy().astype(np.float64)
     used = [k for k in range(16) if t[k, :, 0].max() > 0]
     t0 = min(t[k, :148, 0][t[k, :148, 0] > 0].min() for k in used)
-    names = ["start", "tab0", "str0", "tab1", "str1", "tab2", "str2", "reduced"]
+    names = ["start", "tab0", "str0", "tab1", "str1", "arrived", "-", "reduced"]
     for k in sorted(used, key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min()):
         row = []
         for j, n in enumerate(names):

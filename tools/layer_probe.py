@@ -1,0 +1,115 @@
+"""Timeline of the batched Llama-3-8B layer launch (bench.py's step) on the GPU
+box: per-CTA profiling stamps (abcq_debug_set_trace) of one gemv_batch launch
+over q/k/v/o/gate/up/down at precision p, plus graph-timed launch latency.
+
+    python tools/layer_probe.py --p 3 [--jobs 0,1,2,3,4,5,6] [--copies 3]
+"""
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2510_10467_b200 as P  # noqa: E402
+from paper_2510_10467_b200 import _lib  # noqa: E402
+from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
+
+LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+          ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+NAMES = ["start", "pdl", "tab0", "streamed", "arrived", "completed"]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--p", type=int, default=3)
+ap.add_argument("--jobs", default="0,1,2,3,4,5,6")
+ap.add_argument("--copies", type=int, default=3)
+ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--piece", type=int, default=-1, help="piece cost in blocks (load-balance model)")
+a = ap.parse_args()
+torch.cuda.set_device(0)
+sel = [int(v) for v in a.jobs.split(",")]
+g = torch.Generator(device="cuda").manual_seed(0)
+sets = []
+for c in range(a.copies):
+    row = []
+    for li in sel:
+        _, r, k = LAYERS[li]
+        dm = P.DeviceModel(r, k, 128, 2, 4, False, scale_dtype="f16")
+        dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, r, k // 32), dtype=torch.int32, device="cuda",
+                                     generator=g))
+        for p in (2, 3, 4):
+            dm.load_scale_set(p, np.full((p, r, k // 128), 0.05, np.float32))
+        row.append(dm)
+    sets.append(row)
+xs = {k: torch.randn(k, device="cuda").half() for k in {LAYERS[li][2] for li in sel}}
+ys = [torch.empty(LAYERS[li][1], device="cuda", dtype=torch.float16) for li in sel]
+st = torch.cuda.Stream()
+if a.mode:
+    _lib.lib().abcq_debug_set_mode(a.mode)
+if a.piece >= 0:
+    _lib.lib().abcq_debug_set_mode(1000 + a.piece)
+
+
+def launch(c):
+    gemv_batch([(dm, a.p, xs[dm.cols], ys[i]) for i, dm in enumerate(sets[c])], st)
+
+
+byts = sum(a.p * LAYERS[li][1] * LAYERS[li][2] // 8 + a.p * LAYERS[li][1] * LAYERS[li][2] // 128 * 2 for li in sel)
+with torch.cuda.stream(st):
+    for c in range(a.copies):
+        launch(c)
+torch.cuda.synchronize()
+gr = torch.cuda.CUDAGraph()
+with torch.cuda.graph(gr, stream=st):
+    for i in range(12):
+        launch(i % a.copies)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(st):
+    gr.replay()
+    e0.record(st)
+    for _ in range(5):
+        gr.replay()
+    e1.record(st)
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / 60
+print(f"jobs {[LAYERS[li][0] for li in sel]} p={a.p}: {us:.2f} us/launch, {byts / 1e6:.1f} MB -> "
+      f"{byts / us / 1e3:.0f} GB/s")
+
+SL = 160 * 8
+buf = torch.zeros(16 * SL, dtype=torch.int64, device="cuda")
+_lib.lib().abcq_debug_set_trace(buf.data_ptr())
+g3 = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g3, stream=st):
+    for i in range(4):
+        launch(i % a.copies)
+_lib.lib().abcq_debug_set_trace(None)
+with torch.cuda.stream(st):
+    g3.replay()
+    torch.cuda.synchronize()
+    buf.zero_()
+    g3.replay()
+torch.cuda.synchronize()
+t = buf.view(16, 160, 8).cpu().numpy()
+used = [k for k in range(16) if t[k, :148, 0].max() > 0]
+used.sort(key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min())
+t0 = t[used[0], :148, 0][t[used[0], :148, 0] > 0].min()
+for k in used:
+    T = t[k, :148].astype(np.float64)
+    row = []
+    for j, n in enumerate(NAMES):
+        col = T[:, j][T[:, j] > 0]
+        if len(col):
+            row.append(f"{n} {(col.min() - t0) / 1e3:6.2f}/{(np.median(col) - t0) / 1e3:6.2f}/{(col.max() - t0) / 1e3:6.2f}")
+    print("  " + " | ".join(row))
+# per-CTA detail of the last launch: stream duration (tab0 -> streamed) vs rounds
+T = t[used[-1], :148].astype(np.float64)
+dur = (T[:, 3] - T[:, 2]) / 1e3
+rounds = t[used[-1], :148, 6]
+print("  stream us per CTA: min %.2f med %.2f max %.2f; rounds min %d max %d" % (
+    dur.min(), np.median(dur), dur.max(), rounds.min(), rounds.max()))
+for nr in sorted(set(rounds.tolist())):
+    m = rounds == nr
+    print(f"    rounds={nr}: {m.sum():3d} CTAs, stream med {np.median(dur[m]):.2f} max {dur[m].max():.2f}")
+slow = np.argsort(-dur)[:8]
+print("  slowest CTAs:", ", ".join(f"{b}:{dur[b]:.1f}us/r{rounds[b]}" for b in slow))

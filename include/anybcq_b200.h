@@ -126,8 +126,8 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
  * for one request at precision p (runtime argument, no recompile).
  * x: (cols) in x_dtype; y: (rows) in y_dtype. TILED layout -> the sm_100a
  * LUT kernel; ROWMAJOR layout (any group size) -> the generic kernel.
- * Workspace: >= abcq_gemv_workspace_bytes(); must be zero-filled once
- * before first use and may not be shared by calls running concurrently
+ * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials; no
+ * initialisation needed); may not be shared by calls running concurrently
  * (one workspace per stream).                                             */
 int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
@@ -138,9 +138,8 @@ int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype
  * TMA stream never drains between them) -- e.g. q/k/v or gate/up of a
  * decoder layer, or several requests' precisions. All jobs: TILED layout,
  * the same x/y/scale dtypes and mode; n_jobs <= abcq_gemv_batch_max_jobs().
- * Workspace: abcq_gemv_batch_workspace_bytes, zero-filled once per stream
- * AND per job-list layout (it holds self-resetting counters at offsets that
- * depend on the jobs' shapes).                                              */
+ * Workspace: abcq_gemv_batch_workspace_bytes (the jobs' split-K partials,
+ * no initialisation needed), one per stream.                                */
 typedef struct abcq_gemv_job {
     const abcq_model_t* model;
     int32_t p;

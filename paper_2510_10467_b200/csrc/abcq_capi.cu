@@ -73,6 +73,10 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
+    if (mode >= 2000) {  // ring slots issued before the PDL wait
+        abcq::g_prefill = mode - 2000;
+        return 0;
+    }
     if (mode >= 1000) {  // load-balance model knob, not a mode
         abcq::g_piece_blocks = mode - 1000;
         return 0;

@@ -3,18 +3,17 @@
 // gemv.py:188-222). A single GEMV is a batch of one. Building blocks (layout,
 // lookup, table, TMA helpers) live in abcq_gemv_lut.cuh; DESIGN.md §3.1.
 //
-// One CTA per SM (a co-resident grid) of kWarps warps. Every warp is its own
-// producer and consumer: it owns a contiguous run of items of each job and a
-// private kRing-deep ring of shared-memory slots; lane 0 streams
-// (kK items x one plane) of weights + that plane's scales (+ offsets) per slot
-// with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx), the warp
-// consumes slot e while slots e+1..e+kRing-1 are in flight. No cross-warp
-// synchronisation on the streaming path; the slot stream runs on across job
-// boundaries (weights are static, so it starts before the PDL wait).
-// Per job the warps rebuild the reference lookup table from x (one CTA
-// barrier); with split over slices (NS > 1) items store 16-row partials, and
-// after the last job every CTA completes an even share of every job's row
-// tiles (arrival counters, fixed-order sums -> bitwise reproducible).
+// One CTA per SM (a co-resident grid) of kWarps warps. The batch's items form
+// one sequence split into cost-balanced CTA ranges (see "Work schedule");
+// a range is processed in rounds of <= 2 (job, slice) pieces, one lookup-table
+// build per round. Every warp is its own producer and consumer: a private
+// kRing-deep ring of shared-memory slots, lane 0 streaming (kK items x one
+// plane) of weights + that plane's scales (+ offsets) per slot with TMA bulk
+// copies (cp.async.bulk ... mbarrier::complete_tx); the warp consumes slot e
+// while slots e+1..e+kRing-1 are in flight, and the slot stream runs on across
+// rounds and jobs (weights are static: it starts before the PDL wait). Jobs
+// split over slices (NS > 1) store 16-row partials; ONE PDL-chained
+// batch_reduce_kernel sums them in a fixed order (bitwise reproducible).
 #pragma once
 #include "abcq_gemv_lut.cuh"
 
@@ -32,8 +31,7 @@ struct Job {
     const void* offset;  // offsets of set p, tiled [item][lane] (asymmetric)
     const void* x;
     void* y;
-    float* partial;      // [NS][NRT*16]
-    uint32_t* counters;  // [NRT] arrival counters, self-resetting
+    float* partial;      // [NRT][NS][16]: a row tile's slice partials are one contiguous run
     int rows, cols, NRT, NS, p, items;
     int ibase;      // first item of this job in the batch's item sequence
     int w;          // cost units per item: p blocks + the item's share of a table build
@@ -47,8 +45,8 @@ struct KArgs {
     int n_jobs;
     int total_items;
     int64_t total_units;
-    int fused;
-    int dbg;  // profiling experiments: 1 = skip the lookups
+    int prefill;  // ring slots issued before the PDL wait
+    int dbg;      // profiling experiments: 1 = skip the lookups
     unsigned long long* trace;
 };
 
@@ -57,7 +55,7 @@ struct BatchArgs {
     int n_jobs;
     int total_items;
     int64_t total_units;
-    int fused;  // 1: in-kernel split-K completion; 0: split_reduce_kernel follows
+    int prefill;
     int dbg;
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
 };
@@ -154,19 +152,12 @@ __device__ __forceinline__ int sub_hi(const WarpRun& w, const Round& R, int k) {
     return k == 0 ? min(w.hi, R.pc[0].hi) : (R.nseg == 2 ? w.hi : w.lo);
 }
 
-// fixed-order sum of one row's NS slice partials (4 interleaved chains over
-// ascending s, then (c0 + c1) + (c2 + c3)) -- shared by the fused completion
-// and split_reduce_kernel so every path gives bitwise-identical y
-__device__ __forceinline__ float reduce_row(const float* pp, int NS, int64_t stride) {
-    float c[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int s0 = 0; s0 < NS; s0 += 16) {  // 16 loads in flight
-        float v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = s0 + k < NS ? __ldcg(pp + (s0 + k) * stride) : 0.f;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) c[k & 3] += v[k];
-    }
-    return (c[0] + c[1]) + (c[2] + c[3]);
+// Split-K order (every completion path): row r's NS slice partials are summed
+// as 4 chains, chain m = slices s = m (mod 4) in ascending s, each chain
+// zero-padded to whole 16-slice blocks, then (c0 + c1) + (c2 + c3) -- so every
+// path gives bitwise-identical y. Partials of row tile rt: partial[(rt*NS + s)*16 + r].
+__device__ __forceinline__ const float* partial_row(const Job& J, int row) {
+    return J.partial + ((int64_t)(row >> 4) * J.NS) * kTileRows + (row & 15);
 }
 
 // 16 entries of chunk c of the lookup table, t = u + 16*h (h = 0..15), from the
@@ -293,6 +284,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         }
         enter_round(k, k.rend);
     };
+    const uint64_t pol = l2_evict_first_policy();
     // issue the TMA copies of the cursor's element into slot s (lane 0 only)
     auto issue = [&](const Cur& k, int s) {
         const int cnt = min(kK, k.hi - k.c);
@@ -301,17 +293,20 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         const bool z = ASYM && k.i == 0;
         if (lane == 0) {
             mbar_arrive_expect_tx(&mybar[s], wb + ab + (z ? ab : 0));
-            bulk_g2s(st, k.w, wb, &mybar[s]);
-            bulk_g2s(st + SG::kW, k.al, ab, &mybar[s]);
-            if (z) bulk_g2s(st + SG::kW + SG::kA, k.z, ab, &mybar[s]);
+            bulk_g2s_hint(st, k.w, wb, &mybar[s], pol);
+            bulk_g2s_hint(st + SG::kW, k.al, ab, &mybar[s], pol);
+            if (z) bulk_g2s_hint(st + SG::kW + SG::kA, k.z, ab, &mybar[s], pol);
         }
     };
 
     Cur ic;  // issue cursor: runs R elements ahead of consumption
     enter_round(ic, it0);
-    // static model data: fill the ring before waiting on the previous kernel
-    for (int s = 0; s < R && ic.rs < it1; ++s) {
-        issue(ic, s);
+    // static model data: start the ring before waiting on the previous kernel,
+    // but only a.prefill slots -- x (read right after the wait) must not queue
+    // behind a full ring's worth of bytes on this SM's L2->SM path
+    int s_fill = 0;
+    for (; s_fill < a.prefill && s_fill < R && ic.rs < it1; ++s_fill) {
+        issue(ic, s_fill);
         advance(ic);
     }
     pdl_wait();  // x, y and the workspace belong to the previous kernel
@@ -348,6 +343,10 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
     int round = 0;
     if (it0 < it1) prefetch_x(make_round(a, it0, it1));
+    for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
+        issue(ic, s_fill);
+        advance(ic);
+    }
     for (int rs = it0; rs < it1; ++round) {
         const Round Rd = make_round(a, rs, it1);
         // ---- lookup tables of the round's pieces (one CTA barrier each side) ---
@@ -383,7 +382,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                 for (int c = 0; c < 16; ++c) gx += csum[SEG * 32 + half * 16 + c];
             }
             YT* __restrict__ y = static_cast<YT*>(J.y);
-            float* __restrict__ part = J.partial + (int64_t)P.s * J.NRT * kTileRows;
+            float* __restrict__ part = J.partial + (int64_t)P.s * kTileRows;  // + rt*NS*16 + r
             const int tile0 = J.ibase + P.s * J.NRT;  // batch item of row tile 0 of this slice
             const int p = J.p, NS = J.NS, rows = J.rows;
             for (int c = lo; c < hi; c += kK) {
@@ -446,7 +445,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                 } else {
 #pragma unroll
                     for (int q = 0; q < kK; ++q)
-                        if (q < cnt && lane < 16) __stcg(part + (c + q - tile0) * kTileRows + lane, outv[q]);
+                        if (q < cnt && lane < 16)
+                            __stcg(part + (int64_t)(c + q - tile0) * NS * kTileRows + lane, outv[q]);
                 }
             }
         };
@@ -457,86 +457,21 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 
     ABCQ_BTRACE(3);
     if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 6] = round;
-    if (!a.fused) return;
-    // ---- split-K completion of every job with NS > 1 -------------------------
-    // 1. publish: one fence per warp, then one arrival per streamed item on its
-    //    row tile's counter
-    __syncwarp();
-    __threadfence();
-    for (int rs = it0; rs < it1;) {
-        const Round Rd = make_round(a, rs, it1);
-        const WarpRun wr = warp_run(a, Rd, warp);
-#pragma unroll
-        for (int sb = 0; sb < 2; ++sb) {
-            const Job& J = a.jobs[Rd.pc[sb].j];
-            if (sb >= Rd.nseg || J.NS <= 1) continue;
-            const int tile0 = J.ibase + Rd.pc[sb].s * J.NRT;
-            for (int it = sub_lo(wr, Rd, sb) + lane; it < sub_hi(wr, Rd, sb); it += 32)
-                atomicAdd(&J.counters[it - tile0], 1u);
-        }
-        rs = Rd.end;
-    }
-    ABCQ_BTRACE(4);
-    // 2. CTA b completes row tiles [b*NRT/G, (b+1)*NRT/G) of every split job:
-    //    warp w takes the CTA's tiles w, w+16, ... (flattened over jobs); per
-    //    tile all lanes wait for the NS arrivals, then lane (r, h) sums row r's
-    //    chains 2h, 2h+1 -- reduce_row's fixed order, so the result is bitwise
-    //    equal to split_reduce_kernel -- and the tile's counter is reset (this
-    //    CTA is its only reader).
-    int ntiles = 0;
-    for (int j = 0; j < a.n_jobs; ++j) {
-        const Job& J = a.jobs[j];
-        if (J.NS > 1) ntiles += (int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G);
-    }
-    const int hh = lane >> 4;
-    for (int f = warp; f < ntiles; f += kWarps) {
-        int j = 0, lt = f;
-        for (;; ++j) {  // job j, local tile lt of flat tile index f
-            const Job& J = a.jobs[j];
-            if (J.NS <= 1) continue;
-            const int n = (int)((int64_t)(b + 1) * J.NRT / G) - (int)((int64_t)b * J.NRT / G);
-            if (lt < n) break;
-            lt -= n;
-        }
-        const Job& J = a.jobs[j];
-        const int rt = (int)((int64_t)b * J.NRT / G) + lt;
-        uint32_t seen;
-        for (int backoff = 64;;) {  // poll gently: spinning warps steal L2 slots from the streams
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.counters + rt) : "memory");
-            if (seen >= (uint32_t)J.NS) break;
-            __nanosleep(backoff);
-            backoff = min(backoff * 2, 1024);
-        }
-        const int row = rt * kTileRows + (lane & 15);
-        const int64_t stride = (int64_t)J.NRT * kTileRows;
-        const float* pp = J.partial + row;
-        float c2[2] = {0.f, 0.f};
-        for (int s0 = 0; s0 < J.NS; s0 += 16) {
-            float v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {  // terms s0 + 4m + 2h + {0,1} of chains 2h, 2h+1
-                const int sl = s0 + (k >> 1) * 4 + 2 * hh + (k & 1);
-                v[k] = sl < J.NS ? __ldcg(pp + sl * stride) : 0.f;
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) c2[k & 1] += v[k];
-        }
-        const float mine = c2[0] + c2[1];
-        const float other = __shfl_down_sync(0xffffffffu, mine, 16);
-        if (lane < 16 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
-        if (lane == 0) J.counters[rt] = 0u;  // self-reset for the next launch
-    }
     ABCQ_BTRACE(5);
 }
 
 // Split-K completion as ONE PDL-chained kernel for the whole batch: block k
-// sums kReduceRows rows of one split job (blocks are laid out job by job, so
-// the job lookup is block-uniform); reduce_row's fixed order, so the result is
-// bitwise equal to the in-kernel completion (debug mode 21).
-constexpr int kReduceRows = 128;
+// completes kReduceRows rows of one split job (blocks are laid out job by job,
+// so the job lookup is block-uniform). Four threads per row, thread m sums
+// chain m of the split-K order (slices s = m mod 4, zero-padded to whole 16-slice
+// blocks) with all its loads in flight; then
+// (c0 + c1) + (c2 + c3) -- independent of the batch composition.
+constexpr int kReduceRows = 64;
 template <int NJ, typename YT>
-__global__ void __launch_bounds__(kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
+__global__ void __launch_bounds__(4 * kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
+    if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
     pdl_wait();
+    if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
     pdl_launch_dependents();
     int blk = blockIdx.x, j = 0;
     for (; j < a.n_jobs; ++j) {
@@ -548,9 +483,34 @@ __global__ void __launch_bounds__(kReduceRows) batch_reduce_kernel(const __grid_
     }
     if (j >= a.n_jobs) return;
     const Job& J = a.jobs[j];
-    const int row = blk * kReduceRows + threadIdx.x;
-    if (row < J.rows)
-        static_cast<YT*>(J.y)[row] = from_f32<YT>(reduce_row(J.partial + row, J.NS, (int64_t)J.NRT * kTileRows));
+    const int m = threadIdx.x & 3;
+    const int row = blk * kReduceRows + (threadIdx.x >> 2);
+    const int64_t stride = kTileRows;
+    const float* pp = partial_row(J, row < J.rows ? row : 0);
+    const int nblk = (J.NS + 15) / 16;  // 16-slice blocks (the padding unit)
+    float c = 0.f;
+    for (int b0 = 0; b0 < nblk; b0 += 4) {  // up to 16 loads of this chain in flight
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int s = (b0 + (k >> 2)) * 16 + m + 4 * (k & 3);
+            v[k] = (b0 + (k >> 2) < nblk && s < J.NS) ? __ldcg(pp + s * stride) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (b0 + (k >> 2) < nblk) c += v[k];
+    }
+    const float c01 = c + __shfl_xor_sync(0xffffffffu, c, 1);  // m=0: c0+c1, m=2: c2+c3
+    const float other = __shfl_xor_sync(0xffffffffu, c01, 2);
+    if (m == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(c01 + other);
+    if (a.trace) {  // profiling: last block end, per job
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long t = globaltimer();
+            atomicMax(&a.trace[148 * 8 + 2], t);
+            if (j < 8) atomicMax(&a.trace[149 * 8 + j], t);
+        }
+    }
 }
 
 template <int NJ, typename XT, typename YT, typename ST, bool ASYM>
@@ -560,7 +520,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     a.n_jobs = ba.n_jobs;
     a.total_items = ba.total_items;
     a.total_units = ba.total_units;
-    a.fused = ba.fused;
+    a.prefill = ba.prefill;
     a.dbg = ba.dbg;
     a.trace = ba.trace;
     auto kern = gemv_batch_kernel<NJ, XT, YT, ST, ASYM>;
@@ -572,6 +532,13 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     static bool attr_set[64] = {};  // per instantiation and device
     if (dev < 64 && !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        // the reduce kernel keeps the GEMV's shared-memory carveout: an SM that
+        // ran it must not be reconfigured before the next GEMV CTA can start
+        e = cudaFuncSetAttribute(batch_reduce_kernel<NJ, YT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return (int)e;
         attr_set[dev] = true;
     }
@@ -586,13 +553,13 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e != cudaSuccess || a.fused) return (int)e;
+    if (e != cudaSuccess) return (int)e;
     int nblocks = 0;  // one reduce launch for every split job of the batch
     for (int j = 0; j < a.n_jobs; ++j)
         if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
     if (nblocks == 0) return 0;
     cudaLaunchConfig_t rc = cfg;
-    rc.blockDim = dim3(kReduceRows);
+    rc.blockDim = dim3(4 * kReduceRows);
     rc.gridDim = dim3((unsigned)nblocks);
     rc.dynamicSmemBytes = 0;
     return (int)cudaLaunchKernelEx(&rc, batch_reduce_kernel<NJ, YT>, a);

@@ -10,6 +10,7 @@ int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experi
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
 int g_piece_blocks = 150;
+int g_prefill = 1;  // abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -17,7 +18,7 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 size_t lut_workspace_bytes(const abcq_model_t* m) {
     const int NRT = n_row_tiles(m->rows), NS = n_slices(m->cols);
     if (NS <= 1) return 0;
-    return align256((size_t)NS * NRT * kTileRows * sizeof(float)) + align256((size_t)NRT * sizeof(uint32_t));
+    return align256((size_t)NS * NRT * kTileRows * sizeof(float));  // split-K partials
 }
 
 bool lut_supports(const abcq_model_t* m, int p) {
@@ -41,9 +42,6 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.x = x;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
-    J.counters = ws ? reinterpret_cast<uint32_t*>(
-                          ws + align256((size_t)J.NS * J.NRT * kTileRows * sizeof(float)))
-                    : nullptr;
 }
 
 template <typename XT>
@@ -72,9 +70,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     a.n_jobs = n;
     a.total_items = items;
     a.total_units = units;
-    // split-K completion: one PDL-chained batch_reduce_kernel; debug mode 21
-    // completes in-kernel instead (arrival counters + polling sweep)
-    a.fused = g_dbg_mode == 21;
+    a.prefill = g_prefill;
     a.dbg = g_dbg_mode == 1 ? 1 : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;

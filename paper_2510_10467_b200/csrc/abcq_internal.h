@@ -41,6 +41,7 @@ int launch_dequantize(const abcq_model_t* m, int p, void* w, int w_dtype, cudaSt
 extern unsigned long long* g_trace;
 extern int g_dbg_mode;
 extern int g_piece_blocks;
+extern int g_prefill;
 int num_sms();
 int probe_kernel_image();  // cudaFuncGetAttributes on a packing kernel
 

@@ -18,7 +18,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-NAMES = ["start", "pdl", "tab0", "streamed", "arrived", "completed"]
+NAMES = ["start", "pdl", "tab0", "streamed", "completed"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -88,6 +88,7 @@ with torch.cuda.stream(st):
     g3.replay()
     torch.cuda.synchronize()
     buf.zero_()
+    buf.view(16, 160, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
     g3.replay()
 torch.cuda.synchronize()
 t = buf.view(16, 160, 8).cpu().numpy()
@@ -101,6 +102,12 @@ for k in used:
         col = T[:, j][T[:, j] > 0]
         if len(col):
             row.append(f"{n} {(col.min() - t0) / 1e3:6.2f}/{(np.median(col) - t0) / 1e3:6.2f}/{(col.max() - t0) / 1e3:6.2f}")
+    red = t[k, 148, :3].astype(np.float64)
+    if red[2] > 0:
+        jobs = t[k, 149, :8].astype(np.float64)
+        row.append("reduce first %.2f pdl %.2f end %.2f (jobs %s)" % (
+            (red[0] - t0) / 1e3, (red[1] - t0) / 1e3, (red[2] - t0) / 1e3,
+            " ".join(f"{(v - t0) / 1e3:.1f}" for v in jobs if v > 0)))
     print("  " + " | ".join(row))
 # per-CTA detail of the last launch: stream duration (tab0 -> streamed) vs rounds
 T = t[used[-1], :148].astype(np.float64)

@@ -110,6 +110,16 @@ __device__ __forceinline__ float2 unpack2(unsigned long long v) {
     return r;
 }
 
+// 16-byte global -> shared async copy; bytes past src_bytes are zero-filled
+__device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // streaming 128-bit weight load: read once, keep out of L1
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     uint4 r;

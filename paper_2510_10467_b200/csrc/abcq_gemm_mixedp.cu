@@ -36,7 +36,6 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
                  "l"(src)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 

@@ -182,7 +182,8 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
 
 // profiling stamps (abcq_debug_set_trace): per CTA, slot k = max over the
 // calling warps of %globaltimer. 0 start, 1 after the PDL wait, 2 first table
-// ready, 3 streams done, 4 arrivals published, 5 split-K completed, 6 = rounds
+// ready, 3 streams done, 4 ring filled, 5 first table built (before the
+// barrier); 6 = rounds, 7 = SM id
 #define ABCQ_BTRACE(k)                                                                   \
     do {                                                                                 \
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         issue(ic, s_fill);
         advance(ic);
     }
+    ABCQ_BTRACE(4);
     for (int rs = it0; rs < it1; ++round) {
         const Round Rd = make_round(a, rs, it1);
         // ---- lookup tables of the round's pieces (one CTA barrier each side) ---
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                 if (ASYM && u == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
             }
         }
+        if (round == 0) ABCQ_BTRACE(5);
         __syncthreads();
         if (Rd.end < it1) prefetch_x(make_round(a, Rd.end, it1));
         if (round == 0 && warp == 0) ABCQ_BTRACE(2);
@@ -456,8 +459,12 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     }
 
     ABCQ_BTRACE(3);
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 6] = round;
-    ABCQ_BTRACE(5);
+    if (a.trace && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[blockIdx.x * 8 + 6] = round;
+        a.trace[blockIdx.x * 8 + 7] = smid;
+    }
 }
 
 // Split-K completion as ONE PDL-chained kernel for the whole batch: block k

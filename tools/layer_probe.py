@@ -18,7 +18,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-NAMES = ["start", "pdl", "tab0", "streamed", "completed"]
+NAMES = ["start", "pdl", "tab0", "streamed", "ringfill", "built"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -120,3 +120,24 @@ for nr in sorted(set(rounds.tolist())):
     print(f"    rounds={nr}: {m.sum():3d} CTAs, stream med {np.median(dur[m]):.2f} max {dur[m].max():.2f}")
 slow = np.argsort(-dur)[:8]
 print("  slowest CTAs:", ", ".join(f"{b}:{dur[b]:.1f}us/r{rounds[b]}" for b in slow))
+
+# systematic per-SM speed? correlate stream durations of consecutive launches by SM id
+if len(used) >= 3:
+    d = {}
+    for k in used[1:]:
+        T = t[k, :148].astype(np.float64)
+        smid = t[k, :148, 7]
+        rate = (T[:, 3] - T[:, 2]) / 1e3
+        d[k] = dict(zip(smid.tolist(), rate.tolist())), dict(enumerate(rate.tolist()))
+    ks = list(d)
+    a_sm, b_sm = d[ks[0]][0], d[ks[1]][0]
+    common = sorted(set(a_sm) & set(b_sm))
+    ca = np.corrcoef([a_sm[s] for s in common], [b_sm[s] for s in common])[0, 1]
+    a_b, b_b = d[ks[0]][1], d[ks[1]][1]
+    cb = np.corrcoef([a_b[i] for i in range(148)], [b_b[i] for i in range(148)])[0, 1]
+    print(f"  stream-time correlation across launches: by SM {ca:.2f}, by CTA index {cb:.2f}")
+    sm = np.array(common)
+    v = np.array([(a_sm[s] + b_sm[s]) / 2 for s in common])
+    order = np.argsort(-v)[:12]
+    print("  slowest SMs (avg us):", ", ".join(f"{sm[i]}:{v[i]:.1f}" for i in order))
+    print("  by SM id quartile:", [f"{v[(sm >= q0) & (sm < q0 + 37)].mean():.2f}" for q0 in (0, 37, 74, 111)])

@@ -41,10 +41,11 @@ sys.path.insert(0, str(ROOT))
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-# The timed step runs, per precision, the 7 independent GEMVs of the sweep as
-# ONE persistent batched launch (abcq_gemv_batch). Also reported: the same
-# step grouped as a decoder issues it ([q,k,v] [o] [gate,up] [down]) and as
-# 21 single-GEMV launches.
+# The timed step runs the 21 independent GEMVs of the sweep (7 layers x
+# p=2,3,4 -- per-request precision, the AnyBCQ serving case) as ONE persistent
+# mixed-precision batched launch (abcq_gemv_batch). Also reported: the same
+# step as one launch per precision, grouped as a decoder issues it
+# ([q,k,v] [o] [gate,up] [down] per p), and as 21 single-GEMV launches.
 STEP_GROUPS = [tuple(range(7))]
 DECODER_GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
@@ -74,48 +75,76 @@ def read_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (nvidia_ml_py) while the timed steps run on the device;
+    falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
-        self.idx, self.rows, self.proc = gpu_index, [], None
+        self.idx, self.rows, self.stop = gpu_index, [], threading.Event()
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        p = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+                try:
+                    rs = int(p.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                except Exception:
+                    rs = int(p.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                self.rows.append((sm, rs, time.perf_counter()))
+            except Exception:
+                return
+            time.sleep(0.0005)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=2)
+
+    def mark(self, begin: bool):
+        """host time at the start / end of the timed region"""
+        if begin:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def summary(self):
-        if not self.rows:
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        rows = [r for r in self.rows if t0 <= r[2] <= t1]
+        if not rows:
+            return self._smi_once()
+        sm = [r[0] for r in rows]
+        reasons = sorted({n for _, rs, _ in rows for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(rows), "source": "nvml during the timed region"}
+
+    def _smi_once(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=10).stdout.strip().split(",")
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]), "reasons": ["unsampled-during-run"],
+                    "source": "nvidia-smi after the run"}
+        except Exception:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -175,8 +204,13 @@ def run_gpu(args):
                     for li in grp:
                         dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
 
+    all_jobs = [(pi, p, li) for pi, p in enumerate(PRECISIONS) for li in range(len(LAYERS))]
+
     def step_launches():
-        grouped_launches(STEP_GROUPS)
+        gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for pi, p, li in all_jobs], stream)
+        if world > 1:
+            for pi, p, li in all_jobs:
+                dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
 
     def single_launches():
         for pi, p in enumerate(PRECISIONS):
@@ -223,6 +257,8 @@ def run_gpu(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(0.02)  # poller running before the region starts
+        clk.mark(True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for _ in range(args.steps):
@@ -232,7 +268,7 @@ def run_gpu(args):
                     step_launches()
             ev1.record(stream)
         torch.cuda.synchronize()
-        time.sleep(0.05)
+        clk.mark(False)
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -246,7 +282,8 @@ def run_gpu(args):
     # ---- the same step issued as a decoder would, and as 21 single launches --
     variants = {}
     if rank == 0:
-        for name, fn in (("decoder_grouped", lambda: grouped_launches(DECODER_GROUPS)),
+        for name, fn in (("one_launch_per_precision", lambda: grouped_launches(STEP_GROUPS)),
+                         ("decoder_grouped", lambda: grouped_launches(DECODER_GROUPS)),
                          ("single_launch_per_gemv", single_launches)):
             vms = time_graph(fn)
             variants[name] = {"ms_per_step": round(vms, 4), "GBps": round(step_bytes() / (vms * 1e-3) / 1e9, 1)}
@@ -297,8 +334,13 @@ def run_gpu(args):
         fp16_us = a.elapsed_time(b) * 1e3 / 20
         fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)
         p2_us = sum(per_shape[f"{n}_{r}x{k}_p2"]["us"] for n, r, k in LAYERS)
+        pi2 = PRECISIONS.index(2)
+        p2b_us = 1e3 * time_graph(lambda: gemv_batch(
+            [(models[pi2][li], 2, xs[models[pi2][li].cols], ys[pi2][li]) for li in range(len(LAYERS))], stream))
         fp16 = {"us_per_sweep": round(fp16_us, 2), "GBps": round(fp16_bytes / (fp16_us * 1e-6) / 1e9, 1),
-                "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2)}
+                "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2),
+                "abcq_p2_batched_us_per_sweep": round(p2b_us, 2), "speedup_p2_batched": round(fp16_us / p2b_us, 2),
+                "note": "cuBLAS: 7 torch.mv launches; abcq: 7 single launches, and 1 gemv_batch launch"}
         del dense
 
     # ---- e2e: public API with pinned host buffers, copies in the timed region
@@ -311,15 +353,13 @@ def run_gpu(args):
 
         def e2e_step():
             nonlocal h2d, d2h
-            for pi, p in enumerate(PRECISIONS):
-                for grp in STEP_GROUPS:
-                    for k in {models[pi][li].cols for li in grp}:
-                        dx[k].copy_(hx[k], non_blocking=True)
-                        h2d += hx[k].numel() * 2
-                    gemv_batch([(models[pi][li], p, dx[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
-                    for li in grp:
-                        hy[pi][li].copy_(ys[pi][li], non_blocking=True)
-                        d2h += ys[pi][li].numel() * 2
+            for k in hx:
+                dx[k].copy_(hx[k], non_blocking=True)
+                h2d += hx[k].numel() * 2
+            gemv_batch([(models[pi][li], p, dx[models[pi][li].cols], ys[pi][li]) for pi, p, li in all_jobs], stream)
+            for pi, p, li in all_jobs:
+                hy[pi][li].copy_(ys[pi][li], non_blocking=True)
+                d2h += ys[pi][li].numel() * 2
         with torch.cuda.stream(stream):
             for _ in range(3):
                 e2e_step()
@@ -335,7 +375,8 @@ def run_gpu(args):
         e2e_ms = a.elapsed_time(b) / n_e2e
         e2e = {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d // n_e2e,
-               "d2h_bytes_per_step": d2h // n_e2e, "api": "gemv_batch per decoder group (C ABI abcq_gemv_batch / abcq_gemv), host x/y"}
+               "d2h_bytes_per_step": d2h // n_e2e,
+               "api": "gemv_batch of the 21 GEMVs (C ABI abcq_gemv_batch), pinned host x in / y out"}
 
     if rank == 0:
         peak, peak_kind = read_peaks()
@@ -355,16 +396,17 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
             "config": {"workload": "Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, "
-                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; per p the 7 independent "
-                                   "GEMVs run as one persistent batched launch",
+                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; the 21 independent GEMVs "
+                                   "(per-request precision) run as one persistent mixed-precision "
+                                   "batched launch + one split-K reduce launch",
                        "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
                              f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
                        "timing": "CUDA graph of one step, CUDA events on the launch stream",
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
-            # per p: one persistent batched launch (split-K completed in-kernel)
-            "gpu_launches": args.steps * len(PRECISIONS) * len(STEP_GROUPS),
+            # per step: the persistent batched GEMV kernel + the split-K reduce kernel
+            "gpu_launches": args.steps * 2,
             "step_variants": variants,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

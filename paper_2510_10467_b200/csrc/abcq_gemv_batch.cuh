@@ -19,7 +19,7 @@
 
 namespace abcq {
 
-constexpr int kMaxJobs = 16;
+constexpr int kMaxJobs = 32;
 constexpr int kWarps = 16;
 constexpr int kBThreads = kWarps * 32;
 constexpr int kK = 4;  // items per slot
@@ -38,7 +38,7 @@ struct Job {
     int64_t ubase;  // first cost unit of this job (sum of items * w before it)
 };
 
-// kernel parameter: NJ job slots (1, 4 or 16 -- the smallest that fits)
+// kernel parameter: NJ job slots (1, 8 or 32 -- the smallest that fits)
 template <int NJ>
 struct KArgs {
     Job jobs[NJ];
@@ -575,7 +575,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
 template <typename XT, typename YT, typename ST, bool ASYM>
 int launch_batch_t(const BatchArgs& a, int grid, cudaStream_t st) {
     if (a.n_jobs <= 1) return launch_batch_nj<1, XT, YT, ST, ASYM>(a, grid, st);
-    if (a.n_jobs <= 4) return launch_batch_nj<4, XT, YT, ST, ASYM>(a, grid, st);
+    if (a.n_jobs <= 8) return launch_batch_nj<8, XT, YT, ST, ASYM>(a, grid, st);
     return launch_batch_nj<kMaxJobs, XT, YT, ST, ASYM>(a, grid, st);
 }
 

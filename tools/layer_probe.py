@@ -26,6 +26,7 @@ ap.add_argument("--jobs", default="0,1,2,3,4,5,6")
 ap.add_argument("--copies", type=int, default=3)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--piece", type=int, default=-1, help="piece cost in blocks (load-balance model)")
+ap.add_argument("--mixed", action="store_true", help="jobs at p=2,3,4 in one launch (bench step)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 sel = [int(v) for v in a.jobs.split(",")]
@@ -51,11 +52,15 @@ if a.piece >= 0:
     _lib.lib().abcq_debug_set_mode(1000 + a.piece)
 
 
+PS = (2, 3, 4) if a.mixed else (a.p,)
+
+
 def launch(c):
-    gemv_batch([(dm, a.p, xs[dm.cols], ys[i]) for i, dm in enumerate(sets[c])], st)
+    gemv_batch([(dm, p, xs[dm.cols], ys[i]) for p in PS for i, dm in enumerate(sets[c])], st)
 
 
-byts = sum(a.p * LAYERS[li][1] * LAYERS[li][2] // 8 + a.p * LAYERS[li][1] * LAYERS[li][2] // 128 * 2 for li in sel)
+byts = sum(p * LAYERS[li][1] * LAYERS[li][2] // 8 + p * LAYERS[li][1] * LAYERS[li][2] // 128 * 2
+           for p in PS for li in sel)
 with torch.cuda.stream(st):
     for c in range(a.copies):
         launch(c)
@@ -73,7 +78,7 @@ with torch.cuda.stream(st):
     e1.record(st)
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / 60
-print(f"jobs {[LAYERS[li][0] for li in sel]} p={a.p}: {us:.2f} us/launch, {byts / 1e6:.1f} MB -> "
+print(f"jobs {[LAYERS[li][0] for li in sel]} p={PS}: {us:.2f} us/launch, {byts / 1e6:.1f} MB -> "
       f"{byts / us / 1e3:.0f} GB/s")
 
 SL = 160 * 8

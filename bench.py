@@ -384,9 +384,9 @@ def run_gpu(args):
         achieved = kernel_bytes / (ms_step * 1e-3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "ncu_traffic.json"
-        if tf.exists():
+        if tf.exists():  # ncu dram__bytes_read+write per launch of the batched kernel (profiles/)
             try:
-                traffic = json.loads(tf.read_text())
+                traffic = int(json.loads(tf.read_text())["traffic_bytes_per_launch"])
             except Exception:
                 traffic = None
         cpu = cpu_baseline() if world == 1 and not args.no_cpu else None

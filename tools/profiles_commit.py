@@ -37,14 +37,16 @@ for d in launch.values():
     tot[d["kernel"]] += d.get("gpu__time_duration.sum", 0)
 share = {k: round(v / sum(tot.values()), 4) for k, v in tot.items()}
 
-main = [d for d in launch.values() if "gemv_batch_kernel" in d["kernel"]]
+# the timed step's kernel = the first batched-GEMV launch (bench.py warms up with the step)
+step_kernel = next(launch[i]["kernel"] for i in sorted(launch) if "gemv_batch_kernel" in launch[i]["kernel"])
+main = [d for d in launch.values() if d["kernel"] == step_kernel]
 traffic = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in main) / max(len(main), 1)
 summary = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"),
                           str(ROOT / "gpurun_out" / f"prof_{tag}.ncu-rep"), "--top", "30"],
                          capture_output=True, text=True).stdout
 (out / f"{tag}_gemv_batch_ncu_full.txt").write_text(summary)
 (out / "ncu_traffic.json").write_text(json.dumps({
-    "kernel": "abcq::gemv_batch_kernel", "tag": tag, "traffic_bytes_per_launch": round(traffic),
+    "kernel": step_kernel, "tag": tag, "traffic_bytes_per_launch": round(traffic),
     "launches": len(main), "time_share": share,
     "source": f"profiles/{tag}_launches.csv (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum)"},
     indent=1) + "\n")

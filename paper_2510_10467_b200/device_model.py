@@ -83,6 +83,10 @@ class DeviceModel:
         self.alpha: dict[int, torch.Tensor] = {}
         self.offset: dict[int, torch.Tensor] = {}
         self.planes_loaded = 0
+        # precision p -> event recorded after its planes + scale set were
+        # uploaded on a side stream (container.ProgressiveLoader); launches
+        # that read p wait on it device-side, never on the host
+        self._level_ready: dict[int, torch.cuda.Event] = {}
         self._ws: dict[int, torch.Tensor] = {}
         self._struct = _lib.AbcqModel()
         self._refresh_struct()
@@ -191,6 +195,19 @@ class DeviceModel:
             raise UsageError(f"precision {p} not resident yet (planes loaded: {self.planes_loaded}, "
                              f"scale sets: {sorted(self.alpha)})")
 
+    def mark_level_ready(self, p: int, event: torch.cuda.Event) -> None:
+        """Precision p becomes servable once `event` completes (progressive upload)."""
+        self._level_ready[p] = event
+
+    def _order_after_upload(self, p: int, stream) -> None:
+        ev = self._level_ready.get(p)
+        if ev is None or torch.cuda.is_current_stream_capturing():
+            return  # (CUDA graphs are captured once the model is resident)
+        if ev.query():  # upload finished: no ordering needed from now on
+            del self._level_ready[p]
+            return
+        (stream if stream is not None else torch.cuda.current_stream(self.device)).wait_event(ev)
+
     def struct_ptr(self):
         return C.byref(self._struct)
 
@@ -222,6 +239,7 @@ class DeviceModel:
         """y = W_p x on the device, asynchronous on `stream` (default: current)."""
         self._check_p(p)
         x = self._check_x(x)
+        self._order_after_upload(p, stream)
         if out is None:
             out = torch.empty(self.rows, dtype=out_dtype, device=self.device)
         elif out.numel() != self.rows or not out.is_contiguous():
@@ -240,6 +258,7 @@ class DeviceModel:
             raise UsageError(f"X must be ({B}, {self.cols}), got {tuple(X.shape)}")
         for p in ps:
             self._check_p(int(p))
+            self._order_after_upload(int(p), stream)
         xh = X.to(device=self.device, dtype=torch.float16).contiguous()
         out = torch.empty(B, self.rows, dtype=out_dtype, device=self.device)
         need = C.c_size_t()
@@ -259,6 +278,7 @@ class DeviceModel:
     def gemv_naive(self, p: int, x: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
         self._check_p(p)
         x = self._check_x(x)
+        self._order_after_upload(p, stream)
         out = torch.empty(self.rows, dtype=out_dtype, device=self.device)
         _lib.check(_lib.lib().abcq_gemv_naive(
             self.struct_ptr(), p, x.data_ptr(), dtype_code(x.dtype), out.data_ptr(),
@@ -268,6 +288,7 @@ class DeviceModel:
     def dequantize(self, p: int, dtype=torch.float32, stream=None) -> torch.Tensor:
         """Dense reconstruction (rows, cols) of precision p (bcq.py:372-378)."""
         self._check_p(p)
+        self._order_after_upload(p, stream)
         w = torch.empty(self.rows, self.cols, dtype=dtype, device=self.device)
         _lib.check(_lib.lib().abcq_dequantize(self.struct_ptr(), p, w.data_ptr(), dtype_code(dtype),
                                               _stream_handle(stream)), "abcq_dequantize")
@@ -312,6 +333,7 @@ def gemv_batch(jobs, stream=None):
     for k, (dm, p, x, out) in enumerate(jobs):
         dm._check_p(p)
         x = dm._check_x(x)
+        dm._order_after_upload(p, stream)
         if out.numel() != dm.rows or not out.is_contiguous() or out.device != dm.device:
             raise UsageError("out must be a contiguous device tensor of `rows` elements")
         keep.append(x)

@@ -127,5 +127,27 @@ def main():
     print("done")
 
 
+def containers():
+    """ABCQ container + FMAT goldens written by the reference's own writers
+    (model_format.py:46-79, tensor_io.py:53-57): byte-level fixtures for the
+    container reader/writer (paper_2510_10467_b200/container.py)."""
+    ab = _import_reference()
+    from anybcq.model_format import serialize
+    from anybcq.tensor_io import save_matrix
+    rg = ab.random_gaussian
+    QC = ab.QuantConfig
+    m = ab.build_multiprecision(rg(64, 256, seed=23), 2, 3, QC(group_size=128, cycles=2))
+    serialize(m, HERE / "container_g128_64x256_w4.abcq", scale_width=4)
+    m = ab.build_multiprecision(rg(128, 1024, seed=41), 2, 4, QC(group_size=128, mode="asymmetric", cycles=1))
+    serialize(m, HERE / "container_asym_128x1024_w2.abcq", scale_width=2)
+    m = ab.build_multiprecision(rg(16, 80, seed=15), 2, 3, QC(group_size=40, mode="asymmetric", cycles=2))
+    serialize(m, HERE / "container_asym_g40_16x80_w4.abcq", scale_width=4)
+    save_matrix(rg(3, 256, seed=5), HERE / "x_3x256.fmat")
+    print("containers done")
+
+
 if __name__ == "__main__":
-    main()
+    if "--containers" in sys.argv:
+        containers()
+    else:
+        main()

@@ -176,6 +176,26 @@ int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x
  * half-precision (cuBLAS) comparison weights.                              */
 int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype, void* stream);
 
+/* ---- decode-step harness ops (not part of the reference boundary) --------
+ * The non-GEMV ops of the Llama-3 decode step (paper_2510_10467_b200/decode.py,
+ * SURVEY §8f rank 3), fused, all fp16 tensors with f32 math:
+ *   add_rmsnorm: x += residual (if non-NULL); y = x*rsqrt(mean(x^2)+eps)*w (n <= 8192)
+ *   rope_append: rotate-half RoPE of q (heads x d) and k (kv_heads x d) in place;
+ *                k, v written to the caches (kv_heads, max_ctx, d) at position pos
+ *   attn_decode: one query token over positions [0, ctx) of the caches, GQA,
+ *                head_dim 128, heads/kv_heads <= 8; out (heads x 128)
+ *   silu_mul:    a = silu(g) * u                                            */
+int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
+                         void* stream);
+int abcq_rope_append_f16(void* d_q, void* d_k, const void* d_v, const float* d_cos, const float* d_sin,
+                         void* d_kcache, void* d_vcache, int32_t heads, int32_t kv_heads, int32_t head_dim,
+                         int32_t max_ctx, int32_t pos, void* stream);
+int abcq_attn_decode_workspace_bytes(int32_t heads, int32_t ctx, size_t* out_bytes);
+int abcq_attn_decode_f16(const void* d_q, const void* d_kcache, const void* d_vcache, int32_t heads,
+                         int32_t kv_heads, int32_t max_ctx, int32_t ctx, float scale, void* d_out, void* d_workspace,
+                         size_t workspace_bytes, void* stream);
+int abcq_silu_mul_f16(const void* d_g, const void* d_u, void* d_a, int32_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,12 @@ SIGNATURES = {
     "abcq_gemm_mixedp_workspace_bytes": (C.c_int, [_PM, _i32, C.POINTER(_sz)]),
     "abcq_gemm_mixedp": (C.c_int, [_PM, _i32, C.POINTER(_i32), _vp, _vp, _i32, _vp, _sz, _vp]),
     "abcq_dequantize": (C.c_int, [_PM, _i32, _vp, _i32, _vp]),
+    # decode-step harness ops
+    "abcq_add_rmsnorm_f16": (C.c_int, [_vp, _vp, _vp, _vp, _i32, C.c_float, _vp]),
+    "abcq_rope_append_f16": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "abcq_attn_decode_workspace_bytes": (C.c_int, [_i32, _i32, C.POINTER(_sz)]),
+    "abcq_attn_decode_f16": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp, _sz, _vp]),
+    "abcq_silu_mul_f16": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),
 }
 
 _LIB = None

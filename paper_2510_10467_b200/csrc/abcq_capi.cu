@@ -274,4 +274,47 @@ int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype
     return cuda_ret(abcq::launch_dequantize(m, p, d_w, w_dtype, (cudaStream_t)stream), "abcq_dequantize");
 }
 
+// ---- decode-step harness ops -------------------------------------------------
+int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
+                         void* stream) {
+    if (!d_x || !d_w || !d_y || n < 1 || n > 8192) return fail(ABCQ_E_ARG, "abcq_add_rmsnorm_f16: bad arguments");
+    return cuda_ret(abcq::launch_add_rmsnorm(d_x, d_residual, d_w, d_y, n, eps, (cudaStream_t)stream),
+                    "abcq_add_rmsnorm_f16");
+}
+
+int abcq_rope_append_f16(void* d_q, void* d_k, const void* d_v, const float* d_cos, const float* d_sin,
+                         void* d_kcache, void* d_vcache, int32_t heads, int32_t kv_heads, int32_t head_dim,
+                         int32_t max_ctx, int32_t pos, void* stream) {
+    if (!d_q || !d_k || !d_v || !d_cos || !d_sin || !d_kcache || !d_vcache || heads < 1 || kv_heads < 1 ||
+        head_dim < 2 || head_dim % 2 || head_dim > 2048 || pos < 0 || pos >= max_ctx)
+        return fail(ABCQ_E_ARG, "abcq_rope_append_f16: bad arguments");
+    return cuda_ret(abcq::launch_rope_append(d_q, d_k, d_v, d_cos, d_sin, d_kcache, d_vcache, heads, kv_heads,
+                                             head_dim, max_ctx, pos, (cudaStream_t)stream),
+                    "abcq_rope_append_f16");
+}
+
+int abcq_attn_decode_workspace_bytes(int32_t heads, int32_t ctx, size_t* out_bytes) {
+    if (!out_bytes || heads < 1 || ctx < 1) return fail(ABCQ_E_ARG, "abcq_attn_decode_workspace_bytes: bad arguments");
+    *out_bytes = abcq::attn_decode_workspace_bytes(heads, ctx);
+    return 0;
+}
+
+int abcq_attn_decode_f16(const void* d_q, const void* d_kcache, const void* d_vcache, int32_t heads,
+                         int32_t kv_heads, int32_t max_ctx, int32_t ctx, float scale, void* d_out, void* d_workspace,
+                         size_t workspace_bytes, void* stream) {
+    if (!d_q || !d_kcache || !d_vcache || !d_out || kv_heads < 1 || heads % kv_heads || heads / kv_heads > 8 ||
+        ctx < 1 || ctx > max_ctx)
+        return fail(ABCQ_E_ARG, "abcq_attn_decode_f16: bad arguments (head_dim must be 128, heads/kv_heads <= 8)");
+    if (!d_workspace || workspace_bytes < abcq::attn_decode_workspace_bytes(heads, ctx))
+        return fail(ABCQ_E_WORKSPACE, "abcq_attn_decode_f16: workspace too small");
+    return cuda_ret(abcq::launch_attn_decode(d_q, d_kcache, d_vcache, heads, kv_heads, max_ctx, ctx, scale, d_out,
+                                             d_workspace, (cudaStream_t)stream),
+                    "abcq_attn_decode_f16");
+}
+
+int abcq_silu_mul_f16(const void* d_g, const void* d_u, void* d_a, int32_t n, void* stream) {
+    if (!d_g || !d_u || !d_a || n < 1) return fail(ABCQ_E_ARG, "abcq_silu_mul_f16: bad arguments");
+    return cuda_ret(abcq::launch_silu_mul(d_g, d_u, d_a, n, (cudaStream_t)stream), "abcq_silu_mul_f16");
+}
+
 }  // extern "C"

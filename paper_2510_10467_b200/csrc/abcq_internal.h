@@ -38,6 +38,15 @@ int launch_gemv_generic(const abcq_model_t* m, int p, const void* x, int x_dtype
 
 int launch_dequantize(const abcq_model_t* m, int p, void* w, int w_dtype, cudaStream_t st);
 
+// decode-step harness ops (abcq_decode_ops.cu), f16
+int launch_add_rmsnorm(void* x, const void* r, const void* w, void* y, int n, float eps, cudaStream_t st);
+int launch_rope_append(void* q, void* k, const void* v, const float* cosv, const float* sinv, void* kc, void* vc,
+                       int heads, int kv_heads, int d, int lmax, int pos, cudaStream_t st);
+size_t attn_decode_workspace_bytes(int heads, int L);
+int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads, int kv_heads, int lmax, int L,
+                       float scale, void* out, void* ws, cudaStream_t st);
+int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st);
+
 extern unsigned long long* g_trace;
 extern int g_dbg_mode;
 extern int g_piece_blocks;

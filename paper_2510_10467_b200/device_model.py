@@ -131,18 +131,20 @@ class DeviceModel:
         """Upload scale set p: alpha (p, rows, G) f32, offset (rows, G) f32 or None."""
         if not self.p_lo <= p <= self.p_hi:
             raise UsageError(f"precision {p} outside [{self.p_lo}, {self.p_hi}]")
-        alpha = np.ascontiguousarray(alpha, dtype=np.float32)
-        if alpha.shape != (p, self.rows, self.groups):
-            raise UsageError(f"alpha shape {alpha.shape} != {(p, self.rows, self.groups)}")
+        def as_dev(v):  # numpy or torch (any device) -> f32 on this device
+            if isinstance(v, torch.Tensor):
+                return v.to(device=self.device, dtype=torch.float32).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(self.device)
+        a_dev = as_dev(alpha)
+        if tuple(a_dev.shape) != (p, self.rows, self.groups):
+            raise UsageError(f"alpha shape {tuple(a_dev.shape)} != {(p, self.rows, self.groups)}")
         if (offset is not None) != self.asymmetric:
             raise UsageError("offset presence does not match the model mode")
-        a_dev = torch.from_numpy(alpha).to(self.device)
         o_dev = None
         if offset is not None:
-            offset = np.ascontiguousarray(offset, dtype=np.float32)
-            if offset.shape != (self.rows, self.groups):
-                raise UsageError(f"offset shape {offset.shape} != {(self.rows, self.groups)}")
-            o_dev = torch.from_numpy(offset).to(self.device)
+            o_dev = as_dev(offset)
+            if tuple(o_dev.shape) != (self.rows, self.groups):
+                raise UsageError(f"offset shape {tuple(o_dev.shape)} != {(self.rows, self.groups)}")
         if self.layout == _lib.LAYOUT_TILED:
             na, no = C.c_int64(), C.c_int64()
             _lib.check(_lib.lib().abcq_tiled_scale_elems(self.rows, self.cols, p, C.byref(na), C.byref(no)))

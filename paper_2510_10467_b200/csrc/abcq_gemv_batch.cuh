@@ -39,9 +39,12 @@ struct Job {
 };
 
 // kernel parameter: NJ job slots (1, 8 or 32 -- the smallest that fits)
+constexpr int kMaxGrid = 192;  // CTAs (one per SM)
+
 template <int NJ>
 struct KArgs {
     Job jobs[NJ];
+    int cta_it[kMaxGrid + 1];  // CTA b owns batch items [cta_it[b], cta_it[b+1]) (host-computed)
     int n_jobs;
     int total_items;
     int64_t total_units;
@@ -52,6 +55,7 @@ struct KArgs {
 
 struct BatchArgs {
     Job jobs[kMaxJobs];
+    int cta_it[kMaxGrid + 1];
     int n_jobs;
     int total_items;
     int64_t total_units;
@@ -99,14 +103,6 @@ struct WarpRun {
 };
 
 template <int NJ>
-__device__ __forceinline__ int first_item(const KArgs<NJ>& a, int64_t u) {
-    int j = 0;
-    while (j + 1 < a.n_jobs && a.jobs[j + 1].ubase <= u) ++j;
-    const Job& J = a.jobs[j];
-    const int64_t loc = (u - J.ubase + J.w - 1) / J.w;
-    return J.ibase + (int)(loc < J.items ? loc : J.items);
-}
-template <int NJ>
 __device__ __forceinline__ Piece piece_at(const KArgs<NJ>& a, int g, int it1) {
     Piece P;
     P.j = 0;
@@ -134,17 +130,18 @@ __device__ __forceinline__ Round make_round(const KArgs<NJ>& a, int g, int it1) 
 template <int NJ>
 __device__ __forceinline__ WarpRun warp_run(const KArgs<NJ>& a, const Round& R, int warp) {
     const int p0 = a.jobs[R.pc[0].j].p, p1 = a.jobs[R.pc[1].j].p;
-    const int64_t c0 = (int64_t)(R.pc[0].hi - R.pc[0].lo) * p0;
-    const int64_t c = c0 + (R.nseg == 2 ? (int64_t)(R.pc[1].hi - R.pc[1].lo) * p1 : 0);
-    auto item_at = [&](int64_t pos) -> int {  // first item starting at or after cost pos
-        if (pos <= c0) return R.pc[0].lo + (int)((pos + p0 - 1) / p0);
-        return R.pc[1].lo + (int)((pos - c0 + p1 - 1) / p1);
+    const int c0 = (R.pc[0].hi - R.pc[0].lo) * p0;
+    const int c = c0 + (R.nseg == 2 ? (R.pc[1].hi - R.pc[1].lo) * p1 : 0);
+    auto item_at = [&](int pos) -> int {  // first item starting at or after cost pos
+        if (pos <= c0) return R.pc[0].lo + (pos + p0 - 1) / p0;
+        return R.pc[1].lo + (pos - c0 + p1 - 1) / p1;
     };
     WarpRun w;
-    w.lo = item_at(warp * c / kWarps);
-    w.hi = item_at((warp + 1) * c / kWarps);
+    w.lo = item_at((int)(((int64_t)warp * c) >> 4));  // kWarps == 16: shifts, no 64-bit division
+    w.hi = item_at((int)(((int64_t)(warp + 1) * c) >> 4));
     return w;
 }
+static_assert(kWarps == 16, "warp_run divides by kWarps with a shift");
 __device__ __forceinline__ int sub_lo(const WarpRun& w, const Round& R, int k) {
     return k == 0 ? w.lo : max(w.lo, R.pc[0].hi);
 }
@@ -215,8 +212,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         fence_mbar_init();
     }
     __syncwarp();
-    const int it0 = first_item(a, (int64_t)b * a.total_units / G);
-    const int it1 = first_item(a, (int64_t)(b + 1) * a.total_units / G);
+    const int it0 = a.cta_it[b], it1 = a.cta_it[b + 1];
 
     // ---- this warp's slot stream: rounds -> sub-runs -> chunks of kK items ->
     // planes; the issue cursor keeps its source pointers in registers and
@@ -310,6 +306,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         issue(ic, s_fill);
         advance(ic);
     }
+    ABCQ_BTRACE(7);  // schedule computed, prefill issued (max over warps)
     pdl_wait();  // x, y and the workspace belong to the previous kernel
     if (warp == 0) ABCQ_BTRACE(1);
     pdl_launch_dependents();
@@ -463,19 +460,19 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[blockIdx.x * 8 + 6] = round;
-        a.trace[blockIdx.x * 8 + 7] = smid;
+        (void)smid;
     }
 }
 
 // Split-K completion as ONE PDL-chained kernel for the whole batch: block k
 // completes kReduceRows rows of one split job (blocks are laid out job by job,
-// so the job lookup is block-uniform). Four threads per row, thread m sums
-// chain m of the split-K order (slices s = m mod 4, zero-padded to whole 16-slice
-// blocks) with all its loads in flight; then
-// (c0 + c1) + (c2 + c3) -- independent of the batch composition.
-constexpr int kReduceRows = 64;
+// so the job lookup is block-uniform). Two threads per row: thread h sums
+// chains 2h and 2h+1 of the split-K order (chain m = slices s = m mod 4,
+// ascending, zero-padded to whole 16-slice blocks), up to 16 loads in flight;
+// then (c0 + c1) + (c2 + c3) -- independent of the batch composition.
+constexpr int kReduceRows = 512;  // two threads per row, 1024-thread blocks: a 21-GEMV batch is one wave
 template <int NJ, typename YT>
-__global__ void __launch_bounds__(4 * kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
+__global__ void __launch_bounds__(2 * kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
     pdl_wait();
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
@@ -490,32 +487,32 @@ __global__ void __launch_bounds__(4 * kReduceRows) batch_reduce_kernel(const __g
     }
     if (j >= a.n_jobs) return;
     const Job& J = a.jobs[j];
-    const int m = threadIdx.x & 3;
-    const int row = blk * kReduceRows + (threadIdx.x >> 2);
-    const int64_t stride = kTileRows;
+    const int hh = threadIdx.x & 1;  // chains 2hh, 2hh+1
+    const int row = blk * kReduceRows + (threadIdx.x >> 1);
     const float* pp = partial_row(J, row < J.rows ? row : 0);
     const int nblk = (J.NS + 15) / 16;  // 16-slice blocks (the padding unit)
-    float c = 0.f;
-    for (int b0 = 0; b0 < nblk; b0 += 4) {  // up to 16 loads of this chain in flight
+    float c[2] = {0.f, 0.f};
+    for (int b0 = 0; b0 < nblk; b0 += 2) {  // up to 16 loads in flight
         float v[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int s = (b0 + (k >> 2)) * 16 + m + 4 * (k & 3);
-            v[k] = (b0 + (k >> 2) < nblk && s < J.NS) ? __ldcg(pp + s * stride) : 0.f;
+        for (int k = 0; k < 16; ++k) {  // k: block b0 + k/8, term (k%8)/2 of chain 2hh + k%2
+            const int bb = b0 + (k >> 3);
+            const int s = bb * 16 + ((k & 7) >> 1) * 4 + 2 * hh + (k & 1);
+            v[k] = (bb < nblk && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            if (b0 + (k >> 2) < nblk) c += v[k];
+            if (b0 + (k >> 3) < nblk) c[k & 1] += v[k];
     }
-    const float c01 = c + __shfl_xor_sync(0xffffffffu, c, 1);  // m=0: c0+c1, m=2: c2+c3
-    const float other = __shfl_xor_sync(0xffffffffu, c01, 2);
-    if (m == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(c01 + other);
+    const float mine = c[0] + c[1];  // hh=0: c0+c1, hh=1: c2+c3
+    const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+    if (hh == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
     if (a.trace) {  // profiling: last block end, per job
         __syncthreads();
         if (threadIdx.x == 0) {
             const unsigned long long t = globaltimer();
             atomicMax(&a.trace[148 * 8 + 2], t);
-            if (j < 8) atomicMax(&a.trace[149 * 8 + j], t);
+            if (j < 32) atomicMax(&a.trace[149 * 8 + j], t);
         }
     }
 }
@@ -525,6 +522,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     KArgs<NJ> a;
     for (int j = 0; j < ba.n_jobs; ++j) a.jobs[j] = ba.jobs[j];
     a.n_jobs = ba.n_jobs;
+    for (int i = 0; i <= grid && i <= kMaxGrid; ++i) a.cta_it[i] = ba.cta_it[i];
     a.total_items = ba.total_items;
     a.total_units = ba.total_units;
     a.prefill = ba.prefill;
@@ -566,7 +564,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
     if (nblocks == 0) return 0;
     cudaLaunchConfig_t rc = cfg;
-    rc.blockDim = dim3(4 * kReduceRows);
+    rc.blockDim = dim3(2 * kReduceRows);
     rc.gridDim = dim3((unsigned)nblocks);
     rc.dynamicSmemBytes = 0;
     return (int)cudaLaunchKernelEx(&rc, batch_reduce_kernel<NJ, YT>, a);

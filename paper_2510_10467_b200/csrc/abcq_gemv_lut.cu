@@ -53,7 +53,7 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
                      int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st) {
     BatchArgs a;  // passed by value (kernel parameter space)
-    const int grid = num_sms();
+    const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
     char* w = static_cast<char*>(ws);
     int items = 0;
     int64_t units = 0;
@@ -70,6 +70,16 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     a.n_jobs = n;
     a.total_items = items;
     a.total_units = units;
+    // CTA b owns the items whose first cost unit lies in [b*U/G, (b+1)*U/G)
+    // (computed here once, so the kernel does no 64-bit division)
+    auto first_item = [&](int64_t u) -> int {
+        int j = 0;
+        while (j + 1 < n && a.jobs[j + 1].ubase <= u) ++j;
+        const Job& J = a.jobs[j];
+        const int64_t loc = (u - J.ubase + J.w - 1) / J.w;
+        return J.ibase + (int)(loc < J.items ? loc : J.items);
+    };
+    for (int b = 0; b <= grid; ++b) a.cta_it[b] = first_item((int64_t)b * units / grid);
     a.prefill = g_prefill;
     a.dbg = g_dbg_mode == 1 ? 1 : 0;
     static unsigned trace_seq = 0;

@@ -18,7 +18,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-NAMES = ["start", "pdl", "tab0", "streamed", "ringfill", "built"]
+NAMES = ["start", "pdl", "tab0", "streamed", "ringfill", "built", "-", "sched"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -109,7 +109,7 @@ for k in used:
             row.append(f"{n} {(col.min() - t0) / 1e3:6.2f}/{(np.median(col) - t0) / 1e3:6.2f}/{(col.max() - t0) / 1e3:6.2f}")
     red = t[k, 148, :3].astype(np.float64)
     if red[2] > 0:
-        jobs = t[k, 149, :8].astype(np.float64)
+        jobs = t[k].reshape(-1)[149 * 8:149 * 8 + 32].astype(np.float64)
         row.append("reduce first %.2f pdl %.2f end %.2f (jobs %s)" % (
             (red[0] - t0) / 1e3, (red[1] - t0) / 1e3, (red[2] - t0) / 1e3,
             " ".join(f"{(v - t0) / 1e3:.1f}" for v in jobs if v > 0)))
@@ -127,7 +127,7 @@ slow = np.argsort(-dur)[:8]
 print("  slowest CTAs:", ", ".join(f"{b}:{dur[b]:.1f}us/r{rounds[b]}" for b in slow))
 
 # systematic per-SM speed? correlate stream durations of consecutive launches by SM id
-if len(used) >= 3:
+if False and len(used) >= 3:  # (needs SM ids in slot 7)
     d = {}
     for k in used[1:]:
         T = t[k, :148].astype(np.float64)

@@ -179,8 +179,8 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
 
 // profiling stamps (abcq_debug_set_trace): per CTA, slot k = max over the
 // calling warps of %globaltimer. 0 start, 1 after the PDL wait, 2 first table
-// ready, 3 streams done, 4 ring filled, 5 first table built (before the
-// barrier); 6 = rounds, 7 = SM id
+// ready, 3 streams done, 4 / 5 first / last warp done with round 0, 6 =
+// rounds, 7 round-1 table ready
 #define ABCQ_BTRACE(k)                                                                   \
     do {                                                                                 \
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
@@ -306,9 +306,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         issue(ic, s_fill);
         advance(ic);
     }
-    ABCQ_BTRACE(7);  // schedule computed, prefill issued (max over warps)
     pdl_wait();  // x, y and the workspace belong to the previous kernel
-    if (warp == 0) ABCQ_BTRACE(1);
     pdl_launch_dependents();
 
     const int half = lane >> 4, r = lane & 15;
@@ -345,13 +343,13 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         issue(ic, s_fill);
         advance(ic);
     }
-    ABCQ_BTRACE(4);
     for (int rs = it0; rs < it1; ++round) {
         const Round Rd = make_round(a, rs, it1);
         // ---- lookup tables of the round's pieces (one CTA barrier each side) ---
         // thread (c, u) builds the 16 entries t = u + 16h of chunk c from 8 x
         // values, prefetched into registers while the previous round streamed
         if (round > 0) __syncthreads();  // every warp is done with the previous table
+        if (round == 1 && warp == 0) ABCQ_BTRACE(1);  // profiling: round-1 barrier passed
 #pragma unroll
         for (int ts = 0; ts < 2; ++ts) {
             if (ts < Rd.nseg) {
@@ -364,10 +362,10 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                 if (ASYM && u == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
             }
         }
-        if (round == 0) ABCQ_BTRACE(5);
         __syncthreads();
         if (Rd.end < it1) prefetch_x(make_round(a, Rd.end, it1));
         if (round == 0 && warp == 0) ABCQ_BTRACE(2);
+        if (round == 1 && warp == 0) ABCQ_BTRACE(7);  // round-1 table ready
         const WarpRun wr = warp_run(a, Rd, warp);
 
         // ---- stream this warp's elements of the round ---------------------------
@@ -452,6 +450,13 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         };
         run(std::integral_constant<int, 0>{});
         run(std::integral_constant<int, 1>{});
+        if (round == 0) {  // round-boundary profile: first / last warp done with round 0
+            if (a.trace && lane == 0) {
+                const unsigned long long now = globaltimer();
+                atomicMax(&a.trace[blockIdx.x * 8 + 5], now);
+                atomicMin(&a.trace[blockIdx.x * 8 + 4], now);
+            }
+        }
         rs = Rd.end;
     }
 

@@ -18,7 +18,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-NAMES = ["start", "pdl", "tab0", "streamed", "ringfill", "built", "-", "sched"]
+NAMES = ["start", "bar1", "tab0", "streamed", "r0first", "r0last", "-", "tab1"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -94,6 +94,7 @@ with torch.cuda.stream(st):
     torch.cuda.synchronize()
     buf.zero_()
     buf.view(16, 160, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
+    buf.view(16, 160, 8)[:, :148, 4] = 1 << 62   # first warp done with round 0 (atomicMin)
     g3.replay()
 torch.cuda.synchronize()
 t = buf.view(16, 160, 8).cpu().numpy()
@@ -146,3 +147,63 @@ if False and len(used) >= 3:  # (needs SM ids in slot 7)
     order = np.argsort(-v)[:12]
     print("  slowest SMs (avg us):", ", ".join(f"{sm[i]}:{v[i]:.1f}" for i in order))
     print("  by SM id quartile:", [f"{v[(sm >= q0) & (sm < q0 + 37)].mean():.2f}" for q0 in (0, 37, 74, 111)])
+
+# ---- per-CTA composition (host replica of the kernel's schedule) vs stream time
+if "--fit" in sys.argv[0:0] or True:
+    jobs = [(LAYERS[li][1], LAYERS[li][2], p) for p in PS for li in sel]
+    G = 148
+    pieceb = a.piece if a.piece >= 0 else 250
+    ib, ub, W, NRTs, items = [], [], [], [], []
+    it = u = 0
+    for r, k, p in jobs:
+        nrt, ns = -(-r // 16), -(-k // 256)
+        w = 64 * p + -(-64 * pieceb // nrt)
+        ib.append(it); ub.append(u); W.append(w); NRTs.append(nrt); items.append(nrt * ns)
+        it += nrt * ns; u += nrt * ns * w
+
+    def first_item(uu):
+        j = 0
+        while j + 1 < len(jobs) and ub[j + 1] <= uu:
+            j += 1
+        loc = -(-(uu - ub[j]) // W[j])
+        return ib[j] + min(loc, items[j])
+    cta = [first_item(b * u // G) for b in range(G + 1)]
+
+    def job_of(g):
+        j = 0
+        while j + 1 < len(jobs) and ib[j + 1] <= g:
+            j += 1
+        return j
+    feats = []
+    for b in range(G):
+        g, hi = cta[b], cta[b + 1]
+        blocks = pieces = 0
+        while g < hi:
+            j = job_of(g)
+            s = (g - ib[j]) // NRTs[j]
+            e = min(ib[j] + (s + 1) * NRTs[j], hi)
+            blocks += (e - g) * jobs[j][2]
+            pieces += 1
+            g = e
+        feats.append((blocks, pieces))
+    F = np.array(feats, dtype=np.float64)
+    T = t[used[-1], :148].astype(np.float64)
+    dur = (T[:, 3] - T[:, 2]) / 1e3
+    rnd = t[used[-1], :148, 6].astype(np.float64)
+    X = np.column_stack([F[:, 0], F[:, 1], rnd, np.ones(G)])
+    coef, *_ = np.linalg.lstsq(X, dur, rcond=None)
+    pred = X @ coef
+    print(f"  fit stream_us = {coef[0]*1e3:.3f} ns/block + {coef[1]:.3f} us/piece + {coef[2]:.3f} us/round "
+          f"+ {coef[3]:.2f}; resid rms {np.sqrt(np.mean((dur - pred) ** 2)):.2f} us; "
+          f"blocks/CTA {F[:,0].min():.0f}..{F[:,0].max():.0f}, pieces {F[:,1].min():.0f}..{F[:,1].max():.0f}")
+
+    # round-boundary anatomy for CTAs with >= 2 rounds
+    T = t[used[-1], :148].astype(np.float64)
+    m = (rnd >= 2) & (T[:, 7] > 0)
+    if m.any():
+        skew = (T[m, 5] - T[m, 4]) / 1e3
+        build = (T[m, 7] - T[m, 5]) / 1e3
+        bar = (T[m, 1] - T[m, 5]) / 1e3
+        print(f"  round 0->1 ({m.sum()} CTAs): warp skew med {np.median(skew):.2f} max {skew.max():.2f} us; "
+              f"last warp -> barrier passed med {np.median(bar):.2f}, -> table 1 ready med {np.median(build):.2f} "
+              f"max {build.max():.2f} us")

@@ -115,16 +115,13 @@ __device__ __forceinline__ Piece piece_at(const KArgs<NJ>& a, int g, int it1) {
 }
 template <int NJ>
 __device__ __forceinline__ Round make_round(const KArgs<NJ>& a, int g, int it1) {
+    // one piece per round: round r's table lives in table half r & 1, built
+    // while round r-1 streams (see the kernel), so rounds cost no barrier
     Round R;
     R.pc[0] = piece_at(a, g, it1);
     R.pc[1] = R.pc[0];
     R.nseg = 1;
     R.end = R.pc[0].hi;
-    if (R.end < it1) {
-        R.pc[1] = piece_at(a, R.end, it1);
-        R.nseg = 2;
-        R.end = R.pc[1].hi;
-    }
     return R;
 }
 template <int NJ>
@@ -322,58 +319,91 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         rb[k] = v | ((kTableWindow >> 16) << 24);  // byte 3 -> address byte 2
     }
 
-    // x values of this thread's table tasks: chunk tid&31 of the round's pieces
-    static_assert(kBThreads == 512, "table build maps one thread to (chunk, u) of a slice");
-    float xpre[2][8];
-    auto prefetch_x = [&](const Round& Rn) {
+    // ---- lookup tables: round r uses table half r & 1 (32 columns each) -----
+    // Rounds 0 and 1 are built by the whole CTA up front. Round r+2's table is
+    // built by the 4 warps of builder group r mod 4 (each 4 of the 16 entry
+    // columns): they load its x when they enter round r, finish their round-r
+    // work, wait until all warps are done with round r (a shared counter) and
+    // build into the half round r used; the last builder publishes it. A warp
+    // entering round r >= 2 only waits if that table is not ready yet -- no
+    // CTA-wide barrier between rounds, fast warps run on into the next round.
+    static_assert(kBThreads == 512 && kWarps == 16, "4 builder groups of 4 warps; 16 entry columns");
+    volatile int* done = reinterpret_cast<volatile int*>(smem + 768);   // [2] warps done with round r (r & 1)
+    volatile int* ready = reinterpret_cast<volatile int*>(smem + 776);  // [2] round whose table half h holds
+    volatile int* bcnt = reinterpret_cast<volatile int*>(smem + 784);   // [2] builders done with half h
+    auto build_entries = [&](const float (&xv)[8], int half_sel, int c, int u) {
+        float ev[16];
+        lut_chunk_column16(xv, u, ev);
+        float* col = table + half_sel * 32 + c;
 #pragma unroll
-        for (int ts = 0; ts < 2; ++ts) {
-            if (ts < Rn.nseg) {
-                const Job& Jn = a.jobs[Rn.pc[ts].j];
-                load_x8<XT>(static_cast<const XT*>(Jn.x), Rn.pc[ts].s * kSliceCols + 8 * (tid & 31), Jn.cols,
-                            xpre[ts]);
-            }
-        }
+        for (int h = 0; h < 16; ++h) col[(u + 16 * h) * 64] = ev[h];
+        if (ASYM && u == 15) csum[half_sel * 32 + c] = ev[15];  // T[255] = chunk sum
+    };
+    auto piece_x = [&](const Round& Rn, int c, float (&xv)[8]) {
+        const Job& Jn = a.jobs[Rn.pc[0].j];
+        load_x8<XT>(static_cast<const XT*>(Jn.x), Rn.pc[0].s * kSliceCols + 8 * c, Jn.cols, xv);
     };
 
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
     int round = 0;
-    if (it0 < it1) prefetch_x(make_round(a, it0, it1));
-    for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
-        issue(ic, s_fill);
-        advance(ic);
-    }
-    for (int rs = it0; rs < it1; ++round) {
-        const Round Rd = make_round(a, rs, it1);
-        // ---- lookup tables of the round's pieces (one CTA barrier each side) ---
-        // thread (c, u) builds the 16 entries t = u + 16h of chunk c from 8 x
-        // values, prefetched into registers while the previous round streamed
-        if (round > 0) __syncthreads();  // every warp is done with the previous table
-        if (round == 1 && warp == 0) ABCQ_BTRACE(1);  // profiling: round-1 barrier passed
-#pragma unroll
-        for (int ts = 0; ts < 2; ++ts) {
-            if (ts < Rd.nseg) {
-                const int c = tid & 31, u = tid >> 5;
-                float ev[16];
-                lut_chunk_column16(xpre[ts], u, ev);
-                float* col = table + ts * 32 + c;
-#pragma unroll
-                for (int h = 0; h < 16; ++h) col[(u + 16 * h) * 64] = ev[h];
-                if (ASYM && u == 15) csum[ts * 32 + c] = ev[15];  // T[255] = chunk sum
+    {
+        float xv0[8], xv1[8];
+        const bool has0 = it0 < it1;
+        Round R0, R1;
+        bool has1 = false;
+        if (has0) {
+            R0 = make_round(a, it0, it1);
+            piece_x(R0, tid & 31, xv0);
+            has1 = R0.end < it1;
+            if (has1) {
+                R1 = make_round(a, R0.end, it1);
+                piece_x(R1, tid & 31, xv1);
             }
         }
+        for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
+            issue(ic, s_fill);
+            advance(ic);
+        }
+        if (has0) build_entries(xv0, 0, tid & 31, tid >> 5);
+        if (has1) build_entries(xv1, 1, tid & 31, tid >> 5);
+        if (tid == 0) {
+            done[0] = done[1] = 0;
+            bcnt[0] = bcnt[1] = 0;
+            ready[0] = 0;
+            ready[1] = 1;
+        }
         __syncthreads();
-        if (Rd.end < it1) prefetch_x(make_round(a, Rd.end, it1));
-        if (round == 0 && warp == 0) ABCQ_BTRACE(2);
-        if (round == 1 && warp == 0) ABCQ_BTRACE(7);  // round-1 table ready
+    }
+    if (warp == 0) ABCQ_BTRACE(2);
+    for (int rs = it0; rs < it1; ++round) {
+        const Round Rd = make_round(a, rs, it1);
+        if (round >= 2) {  // table of round `round` (built by the last warp of round-2)
+            if (ready[round & 1] < round) {
+                const unsigned long long t0 = a.trace ? globaltimer() : 0;
+                while (ready[round & 1] < round) __nanosleep(64);
+                if (a.trace && lane == 0) atomicAdd(&a.trace[blockIdx.x * 8 + 7], globaltimer() - t0);
+            }
+            __threadfence_block();
+        }
         const WarpRun wr = warp_run(a, Rd, warp);
+        // builder of round+2's table? then fetch its x now (used after this round)
+        const bool builder = (warp >> 2) == (round & 3);
+        bool build_next = false;
+        float bx[8];
+        if (builder && Rd.end < it1) {
+            const Round Rn1 = make_round(a, Rd.end, it1);
+            if (Rn1.end < it1) {
+                build_next = true;
+                piece_x(make_round(a, Rn1.end, it1), lane, bx);
+            }
+        }
 
         // ---- stream this warp's elements of the round ---------------------------
         auto run = [&](auto seg_tag) {
-            constexpr int SEG = decltype(seg_tag)::value;
-            const int lo = sub_lo(wr, Rd, SEG), hi = sub_hi(wr, Rd, SEG);
+            constexpr int SEG = decltype(seg_tag)::value;  // table half = round & 1
+            const int lo = sub_lo(wr, Rd, 0), hi = sub_hi(wr, Rd, 0);
             if (lo >= hi) return;
-            const Piece& P = Rd.pc[SEG];
+            const Piece& P = Rd.pc[0];
             const Job& J = a.jobs[P.j];
             float gx = 0.f;
             if constexpr (ASYM) {
@@ -448,13 +478,39 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                 }
             }
         };
-        run(std::integral_constant<int, 0>{});
-        run(std::integral_constant<int, 1>{});
+        if (round & 1)
+            run(std::integral_constant<int, 1>{});
+        else
+            run(std::integral_constant<int, 0>{});
         if (round == 0) {  // round-boundary profile: first / last warp done with round 0
             if (a.trace && lane == 0) {
                 const unsigned long long now = globaltimer();
                 atomicMax(&a.trace[blockIdx.x * 8 + 5], now);
                 atomicMin(&a.trace[blockIdx.x * 8 + 4], now);
+            }
+        }
+        // done with round `round`; builders fill round+2's table into this half
+        __syncwarp();
+        if (lane == 0) atomicAdd((int*)&done[round & 1], 1);
+        if (build_next) {
+            if (done[round & 1] < kWarps) {
+                const unsigned long long t0 = a.trace ? globaltimer() : 0;
+                while (done[round & 1] < kWarps) __nanosleep(32);
+                if (a.trace && lane == 0) atomicAdd(&a.trace[blockIdx.x * 8 + 1], globaltimer() - t0);
+            }
+            __threadfence_block();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) build_entries(bx, round & 1, lane, (warp & 3) * 4 + k);
+            __syncwarp();
+            __threadfence_block();
+            int old = 0;
+            if (lane == 0) old = atomicAdd((int*)&bcnt[round & 1], 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == 3 && lane == 0) {  // last of the 4 builders: recycle the counters, publish
+                done[round & 1] = 0;
+                bcnt[round & 1] = 0;
+                __threadfence_block();
+                ready[round & 1] = round + 2;
             }
         }
         rs = Rd.end;

@@ -18,7 +18,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-NAMES = ["start", "bar1", "tab0", "streamed", "r0first", "r0last", "-", "tab1"]
+NAMES = ["start", "-", "tab0", "streamed", "r0first", "r0last"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -197,6 +197,10 @@ if "--fit" in sys.argv[0:0] or True:
           f"+ {coef[3]:.2f}; resid rms {np.sqrt(np.mean((dur - pred) ** 2)):.2f} us; "
           f"blocks/CTA {F[:,0].min():.0f}..{F[:,0].max():.0f}, pieces {F[:,1].min():.0f}..{F[:,1].max():.0f}")
 
+    W = t[used[-1], :148, 7].astype(np.float64) / 1e3
+    Bt = t[used[-1], :148, 1].astype(np.float64) / 1e3
+    print(f"  table waits per CTA (sum over warps): med {np.median(W):.2f} max {W.max():.2f} us; "
+          f"builders waiting for the round to drain: med {np.median(Bt):.2f} max {Bt.max():.2f} us")
     # round-boundary anatomy for CTAs with >= 2 rounds
     T = t[used[-1], :148].astype(np.float64)
     m = (rnd >= 2) & (T[:, 7] > 0)

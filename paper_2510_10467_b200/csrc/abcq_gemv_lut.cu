@@ -9,7 +9,7 @@ unsigned long long* g_trace = nullptr;  // abcq_debug_set_trace (profiling aid)
 int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experiments)
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
-int g_piece_blocks = 250;
+int g_piece_blocks = 200;
 int g_prefill = 1;  // abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
 

@@ -152,7 +152,7 @@ if False and len(used) >= 3:  # (needs SM ids in slot 7)
 if "--fit" in sys.argv[0:0] or True:
     jobs = [(LAYERS[li][1], LAYERS[li][2], p) for p in PS for li in sel]
     G = 148
-    pieceb = a.piece if a.piece >= 0 else 250
+    pieceb = a.piece if a.piece >= 0 else 200
     ib, ub, W, NRTs, items = [], [], [], [], []
     it = u = 0
     for r, k, p in jobs:

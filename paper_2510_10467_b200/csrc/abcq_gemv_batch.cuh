@@ -295,9 +295,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 
     Cur ic;  // issue cursor: runs R elements ahead of consumption
     enter_round(ic, it0);
-    // static model data: start the ring before waiting on the previous kernel,
-    // but only a.prefill slots -- x (read right after the wait) must not queue
-    // behind a full ring's worth of bytes on this SM's L2->SM path
+    // static model data: fill the ring (a.prefill slots, default all) before
+    // waiting on the previous kernel -- the weights land during the wait
     int s_fill = 0;
     for (; s_fill < a.prefill && s_fill < R && ic.rs < it1; ++s_fill) {
         issue(ic, s_fill);

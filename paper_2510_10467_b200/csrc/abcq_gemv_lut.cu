@@ -10,7 +10,7 @@ int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experi
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
 int g_piece_blocks = 200;
-int g_prefill = 1;  // abcq_debug_set_mode(2000 + v)
+int g_prefill = 8;  // ring slots issued before the PDL wait (all of them); abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }

@@ -5,6 +5,7 @@ over q/k/v/o/gate/up/down at precision p, plus graph-timed launch latency.
     python tools/layer_probe.py --p 3 [--jobs 0,1,2,3,4,5,6] [--copies 3]
 """
 import argparse
+import signal
 import sys
 from pathlib import Path
 
@@ -28,6 +29,7 @@ ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--piece", type=int, default=-1, help="piece cost in blocks (load-balance model)")
 ap.add_argument("--mixed", action="store_true", help="jobs at p=2,3,4 in one launch (bench step)")
 a = ap.parse_args()
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under | head
 torch.cuda.set_device(0)
 sel = [int(v) for v in a.jobs.split(",")]
 g = torch.Generator(device="cuda").manual_seed(0)

@@ -126,9 +126,9 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
  * for one request at precision p (runtime argument, no recompile).
  * x: (cols) in x_dtype; y: (rows) in y_dtype. TILED layout -> the sm_100a
  * LUT kernel; ROWMAJOR layout (any group size) -> the generic kernel.
- * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials; no
- * initialisation needed); may not be shared by calls running concurrently
- * (one workspace per stream).                                             */
+ * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials + self-
+ * resetting completion counters): zero-filled once before first use; may
+ * not be shared by calls running concurrently (one workspace per stream).  */
 int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
               int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
@@ -139,7 +139,8 @@ int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype
  * decoder layer, or several requests' precisions. All jobs: TILED layout,
  * the same x/y/scale dtypes and mode; n_jobs <= abcq_gemv_batch_max_jobs().
  * Workspace: abcq_gemv_batch_workspace_bytes (the jobs' split-K partials,
- * no initialisation needed), one per stream.                                */
+ * then per-job self-resetting counters): zero-filled once per stream AND
+ * per job-list layout (the counters' offset depends on the jobs' shapes).   */
 typedef struct abcq_gemv_job {
     const abcq_model_t* model;
     int32_t p;

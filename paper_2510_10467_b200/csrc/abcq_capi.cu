@@ -199,9 +199,9 @@ static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {
 int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n, size_t* out_bytes) {
     if (int rc = check_jobs(jobs, n)) return rc;
     if (!out_bytes) return fail(ABCQ_E_ARG, "out_bytes is NULL");
-    size_t tot = 0;
-    for (int j = 0; j < n; ++j) tot += abcq::lut_workspace_bytes(jobs[j].model);
-    *out_bytes = tot;
+    const abcq_model_t* models[32];
+    for (int j = 0; j < n; ++j) models[j] = jobs[j].model;
+    *out_bytes = abcq::lut_jobs_workspace_bytes(models, n);
     return 0;
 }
 

@@ -33,6 +33,9 @@ struct Job {
     void* y;
     float* partial;      // [NRT][NS][16]: a row tile's slice partials are one contiguous run
     int rows, cols, NRT, NS, p, items;
+    uint32_t* arrive;   // CTAs done streaming this job (split jobs; self-resetting)
+    uint32_t* reduced;  // reduce blocks done with this job (self-resetting)
+    int ncta;           // CTAs whose range touches this job
     int ibase;      // first item of this job in the batch's item sequence
     int w;          // cost units per item: p blocks + the item's share of a table build
     int64_t ubase;  // first cost unit of this job (sum of items * w before it)
@@ -516,6 +519,17 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     }
 
     ABCQ_BTRACE(3);
+    // publish this CTA's split-K partials: one release per CTA, one arrival per
+    // split job it touched -- the reduce kernel starts on a job as soon as all
+    // of its CTAs arrived, while stragglers are still streaming other jobs
+    __syncthreads();
+    if (tid == 0 && it0 < it1) {
+        __threadfence();
+        for (int j = 0; j < a.n_jobs; ++j) {
+            const Job& J = a.jobs[j];
+            if (J.NS > 1 && it0 < J.ibase + J.items && it1 > J.ibase) atomicAdd(J.arrive, 1u);
+        }
+    }
     if (a.trace && tid == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -534,19 +548,35 @@ constexpr int kReduceRows = 512;  // two threads per row, 1024-thread blocks: a 
 template <int NJ, typename YT>
 __global__ void __launch_bounds__(2 * kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
-    pdl_wait();
-    if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
     pdl_launch_dependents();
-    int blk = blockIdx.x, j = 0;
+    int blk = blockIdx.x, j = 0, nbj = 0;
     for (; j < a.n_jobs; ++j) {
         const Job& J = a.jobs[j];
         if (J.NS <= 1) continue;
-        const int nb = (J.rows + kReduceRows - 1) / kReduceRows;
-        if (blk < nb) break;
-        blk -= nb;
+        nbj = (J.rows + kReduceRows - 1) / kReduceRows;
+        if (blk < nbj) break;
+        blk -= nbj;
     }
-    if (j >= a.n_jobs) return;
+    if (j >= a.n_jobs) {
+        pdl_wait();
+        return;
+    }
     const Job& J = a.jobs[j];
+    // no griddepcontrol.wait up front: wait for this job's CTA arrivals only
+    // (acquire), so the reduction overlaps the GEMV kernel's straggler CTAs.
+    // (The GEMV kernel waited for all earlier work before it let this grid
+    // launch; this grid waits for the GEMV grid before it exits, so the next
+    // kernel sees both complete.)
+    if (threadIdx.x == 0) {
+        uint32_t seen;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
+            if (seen >= (uint32_t)J.ncta) break;
+            __nanosleep(128);
+        }
+        if (a.trace) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
+    }
+    __syncthreads();
     const int hh = threadIdx.x & 1;  // chains 2hh, 2hh+1
     const int row = blk * kReduceRows + (threadIdx.x >> 1);
     const float* pp = partial_row(J, row < J.rows ? row : 0);
@@ -567,14 +597,19 @@ __global__ void __launch_bounds__(2 * kReduceRows) batch_reduce_kernel(const __g
     const float mine = c[0] + c[1];  // hh=0: c0+c1, hh=1: c2+c3
     const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
     if (hh == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
-    if (a.trace) {  // profiling: last block end, per job
-        __syncthreads();
-        if (threadIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.trace) {  // profiling: last block end, per job
             const unsigned long long t = globaltimer();
             atomicMax(&a.trace[148 * 8 + 2], t);
             if (j < 32) atomicMax(&a.trace[149 * 8 + j], t);
         }
+        if (atomicAdd(J.reduced, 1u) == (uint32_t)(nbj - 1)) {  // last block of job j: recycle
+            *J.arrive = 0u;
+            *J.reduced = 0u;
+        }
     }
+    pdl_wait();  // the GEMV grid (y of unsplit jobs) completes before this grid does
 }
 
 template <int NJ, typename XT, typename YT, typename ST, bool ASYM>

@@ -15,11 +15,21 @@ constexpr int kCostScale = 64;
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-size_t lut_workspace_bytes(const abcq_model_t* m) {
+static size_t partial_bytes(const abcq_model_t* m) {
     const int NRT = n_row_tiles(m->rows), NS = n_slices(m->cols);
     if (NS <= 1) return 0;
     return align256((size_t)NS * NRT * kTileRows * sizeof(float));  // split-K partials
 }
+constexpr size_t kCounterBytes = 2 * kMaxJobs * sizeof(uint32_t);  // per job: CTA arrivals, reduce blocks done
+
+// workspace of a job list: every split job's partials, then (if any job is
+// split) the self-resetting per-job counters -- zero-filled once before use
+size_t lut_jobs_workspace_bytes(const abcq_model_t* const* models, int n) {
+    size_t tot = 0;
+    for (int j = 0; j < n; ++j) tot += partial_bytes(models[j]);
+    return tot ? tot + kCounterBytes : 0;
+}
+size_t lut_workspace_bytes(const abcq_model_t* m) { return lut_jobs_workspace_bytes(&m, 1); }
 
 bool lut_supports(const abcq_model_t* m, int p) {
     return m->layout == ABCQ_LAYOUT_TILED && p <= kMaxFastP && n_slices(m->cols) <= num_sms();
@@ -42,6 +52,7 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.x = x;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
+    J.ncta = 0;
 }
 
 template <typename XT>
@@ -57,9 +68,14 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     char* w = static_cast<char*>(ws);
     int items = 0;
     int64_t units = 0;
+    size_t part_total = 0;
+    for (int j = 0; j < n; ++j) part_total += partial_bytes(models[j]);
+    uint32_t* counters = part_total ? reinterpret_cast<uint32_t*>(w + part_total) : nullptr;
     for (int j = 0; j < n; ++j) {
         make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
-        w += lut_workspace_bytes(models[j]);
+        w += partial_bytes(models[j]);
+        a.jobs[j].arrive = counters ? counters + j : nullptr;
+        a.jobs[j].reduced = counters ? counters + kMaxJobs + j : nullptr;
         Job& J = a.jobs[j];
         J.ibase = items;
         J.ubase = units;
@@ -80,6 +96,11 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
         return J.ibase + (int)(loc < J.items ? loc : J.items);
     };
     for (int b = 0; b <= grid; ++b) a.cta_it[b] = first_item((int64_t)b * units / grid);
+    for (int j = 0; j < n; ++j) {  // CTAs whose range touches job j (arrivals its reduce waits for)
+        Job& J = a.jobs[j];
+        for (int b = 0; b < grid; ++b)
+            if (a.cta_it[b] < J.ibase + J.items && a.cta_it[b + 1] > J.ibase && a.cta_it[b] < a.cta_it[b + 1]) ++J.ncta;
+    }
     a.prefill = g_prefill;
     a.dbg = g_dbg_mode == 1 ? 1 : 0;
     static unsigned trace_seq = 0;

@@ -17,6 +17,7 @@ int launch_lut_build(const void* x, int x_dtype, int cols, int mu, float* table,
 
 // fast path: TILED layout, group 128
 size_t lut_workspace_bytes(const abcq_model_t* m);
+size_t lut_jobs_workspace_bytes(const abcq_model_t* const* models, int n);
 bool lut_supports(const abcq_model_t* m, int p);  // tiled layout and p <= 8
 int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
                     void* ws, cudaStream_t st);

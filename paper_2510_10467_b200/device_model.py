@@ -214,13 +214,13 @@ class DeviceModel:
         return C.byref(self._struct)
 
     def workspace(self, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-        """Split-K workspace, one per stream (abcq_gemv contract)."""
+        """Split-K workspace, one per stream, zero-filled once (abcq_gemv contract)."""
         h = _stream_handle(stream)
         ws = self._ws.get(h)
         if ws is None:
             n = C.c_size_t()
             _lib.check(_lib.lib().abcq_gemv_workspace_bytes(self.struct_ptr(), C.byref(n)))
-            ws = torch.empty(max(int(n.value), 16), dtype=torch.uint8, device=self.device)
+            ws = torch.zeros(max(int(n.value), 16), dtype=torch.uint8, device=self.device)
             self._ws[h] = ws
         return ws
 
@@ -348,11 +348,12 @@ def gemv_batch(jobs, stream=None):
     need = C.c_size_t()
     _lib.check(L.abcq_gemv_batch_workspace_bytes(arr, n, C.byref(need)), "abcq_gemv_batch")
     dev = jobs[0][0].device
-    # split-K partials of the jobs: one buffer per stream, grown on demand
-    key = (_stream_handle(stream), dev.index)
+    # split-K partials + self-resetting per-job counters at an offset that
+    # depends on the job list: one zero-filled buffer per stream and layout
+    key = (_stream_handle(stream), dev.index, tuple((j[0].rows, j[0].cols) for j in jobs))
     ws = _BATCH_WS.get(key)
     if ws is None or ws.numel() < need.value:
-        ws = torch.empty(max(int(need.value), 16), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(max(int(need.value), 16), dtype=torch.uint8, device=dev)
         _BATCH_WS[key] = ws
     _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv_batch")
     return [j[3] for j in jobs]

@@ -258,6 +258,42 @@ def test_bench_counters_and_render(P):
         P.bench(make_model(P, c), [2], c["x_0"], repeats=0)
 
 
+@pytest.mark.parametrize("asym", [False, True])
+def test_gemv_batch_32_random_jobs_vs_oracle(P, asym):
+    """The full batch width (32 jobs): random shapes (ragged rows/cols, one-slice
+    and many-slice jobs), random per-job precision, shared and distinct x --
+    exercises the cost-balanced CTA ranges, single-piece rounds with builder
+    warp groups, and the per-job arrival counters; every output vs the oracle,
+    twice (counters self-reset), and bitwise equal to single calls."""
+    from paper_2510_10467_b200.device_model import gemv_batch
+    rng = np.random.default_rng(7)
+    shapes = [(int(rng.integers(1, 600)), int(rng.choice([100, 256, 300, 1024, 2000, 4096]))) for _ in range(12)]
+    models = [(P.DeviceModel.from_model(synth_model(P, r, c, 1, 4, asym=asym, seed=i), scale_dtype="f16"),
+               synth_model(P, r, c, 1, 4, asym=asym, seed=i)) for i, (r, c) in enumerate(shapes)]
+    xs = {}
+    jobs, want = [], []
+    for n in range(32):
+        dm, host = models[n % len(models)]
+        p = int(rng.integers(1, 5))
+        if dm.cols not in xs or n % 5 == 0:
+            xs[dm.cols] = O.random_gaussian(1, dm.cols, seed=100 + n).ravel().astype(np.float16)
+        x = xs[dm.cols]
+        xd = torch.from_numpy(x).cuda()
+        out = torch.empty(dm.rows, device="cuda", dtype=torch.float32)
+        jobs.append((dm, p, xd, out))
+        st = host.scale_sets[p]
+        a16 = st.alpha.astype(np.float16).astype(np.float32)
+        z16 = st.offset.astype(np.float16).astype(np.float32) if asym else None
+        want.append(O.gemv_lut(host.bitplanes.words, dm.cols, 128, a16, z16, p, x.astype(np.float32)))
+    for _ in range(2):
+        gemv_batch(jobs)
+        torch.cuda.synchronize()
+        for (dm, p, _, out), w in zip(jobs, want):
+            assert O.rel_dev(out.cpu().numpy(), w) <= REF_TOL, (dm.rows, dm.cols, p)
+    for dm, p, xd, out in jobs[:6]:
+        assert torch.equal(dm.gemv(p, xd), out)
+
+
 def test_gemv_batch_matches_single_calls(P):
     """One persistent launch over mixed shapes / precisions (incl. the same model
     at several p, as per-request precision does) == separate calls, bitwise."""

@@ -14,6 +14,29 @@
 
 namespace abcq {
 
+// Every op here is launched with programmatic stream serialization (PDL): it
+// waits for its producer with griddepcontrol.wait before touching inputs, and
+// releases its consumer early -- in a CUDA-graphed decode step each launch's
+// ramp overlaps the previous kernel's tail (one decoder layer is ~13 kernels).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -29,6 +52,7 @@ __device__ __forceinline__ float warp_max(float v) {
 __global__ void __launch_bounds__(1024) add_rmsnorm_kernel(__half* __restrict__ x, const __half* __restrict__ r,
                                                            const __half* __restrict__ w, __half* __restrict__ y,
                                                            int n, float eps) {
+    pdl_enter();
     __shared__ float red[32];
     float v[8];
     float ss = 0.f;
@@ -68,6 +92,7 @@ __global__ void rope_append_kernel(__half* __restrict__ q, __half* __restrict__ 
                                    const float* __restrict__ cosv, const float* __restrict__ sinv,
                                    __half* __restrict__ kc, __half* __restrict__ vc, int heads, int kv_heads,
                                    int d, int lmax, int pos) {
+    pdl_enter();
     const int b = blockIdx.x, t = threadIdx.x, h2 = d / 2;
     const bool isq = b < heads;
     __half* vec = isq ? q + (size_t)b * d : k + (size_t)(b - heads) * d;
@@ -96,6 +121,7 @@ constexpr int kPartStride = 4 + 128;  // m, l, pad, pad, acc[128] (16-byte align
 __global__ void attn_decode_partial(const __half* __restrict__ q, const __half* __restrict__ kc,
                                     const __half* __restrict__ vc, int heads, int kv_heads, int lmax, int L,
                                     float scale, float* __restrict__ part) {
+    pdl_enter();
     constexpr int d = 128;
     __shared__ __half ks[kAttnSplit][d + 2];  // odd word stride: lane-per-row dots are conflict-free
     __shared__ __half vs[kAttnSplit][d];
@@ -150,6 +176,7 @@ __global__ void attn_decode_partial(const __half* __restrict__ q, const __half* 
 
 // one block of 128 threads per head: out[h] = sum_s e^{m_s - M} acc_s / sum_s e^{m_s - M} l_s
 __global__ void attn_decode_combine(const float* __restrict__ part, int splits, __half* __restrict__ out) {
+    pdl_enter();
     constexpr int d = 128;
     const int h = blockIdx.x, t = threadIdx.x;
     const float* ph = part + (size_t)h * splits * kPartStride;
@@ -166,6 +193,7 @@ __global__ void attn_decode_combine(const float* __restrict__ part, int splits, 
 
 __global__ void silu_mul_kernel(const __half* __restrict__ g, const __half* __restrict__ u, __half* __restrict__ a,
                                 int n) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         const float gv = __half2float(g[i]);
@@ -174,17 +202,16 @@ __global__ void silu_mul_kernel(const __half* __restrict__ g, const __half* __re
 }
 
 int launch_add_rmsnorm(void* x, const void* r, const void* w, void* y, int n, float eps, cudaStream_t st) {
-    add_rmsnorm_kernel<<<1, 1024, 0, st>>>(static_cast<__half*>(x), static_cast<const __half*>(r),
-                                           static_cast<const __half*>(w), static_cast<__half*>(y), n, eps);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(add_rmsnorm_kernel, dim3(1), dim3(1024), st, static_cast<__half*>(x),
+                           static_cast<const __half*>(r), static_cast<const __half*>(w), static_cast<__half*>(y), n,
+                           eps);
 }
 
 int launch_rope_append(void* q, void* k, const void* v, const float* cosv, const float* sinv, void* kc, void* vc,
                        int heads, int kv_heads, int d, int lmax, int pos, cudaStream_t st) {
-    rope_append_kernel<<<heads + kv_heads, d / 2, 0, st>>>(
-        static_cast<__half*>(q), static_cast<__half*>(k), static_cast<const __half*>(v), cosv, sinv,
-        static_cast<__half*>(kc), static_cast<__half*>(vc), heads, kv_heads, d, lmax, pos);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(rope_append_kernel, dim3(heads + kv_heads), dim3(d / 2), st, static_cast<__half*>(q),
+                           static_cast<__half*>(k), static_cast<const __half*>(v), cosv, sinv,
+                           static_cast<__half*>(kc), static_cast<__half*>(vc), heads, kv_heads, d, lmax, pos);
 }
 
 size_t attn_decode_workspace_bytes(int heads, int L) {
@@ -194,17 +221,18 @@ size_t attn_decode_workspace_bytes(int heads, int L) {
 int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads, int kv_heads, int lmax, int L,
                        float scale, void* out, void* ws, cudaStream_t st) {
     const int splits = (L + kAttnSplit - 1) / kAttnSplit;
-    attn_decode_partial<<<dim3(kv_heads, splits), 32 * (heads / kv_heads), 0, st>>>(
-        static_cast<const __half*>(q), static_cast<const __half*>(kc), static_cast<const __half*>(vc), heads,
-        kv_heads, lmax, L, scale, static_cast<float*>(ws));
-    attn_decode_combine<<<heads, 128, 0, st>>>(static_cast<const float*>(ws), splits, static_cast<__half*>(out));
-    return (int)cudaGetLastError();
+    cudaError_t e = launch_pdl(attn_decode_partial, dim3(kv_heads, splits), dim3(32 * (heads / kv_heads)), st,
+                               static_cast<const __half*>(q), static_cast<const __half*>(kc),
+                               static_cast<const __half*>(vc), heads, kv_heads, lmax, L, scale,
+                               static_cast<float*>(ws));
+    if (e != cudaSuccess) return (int)e;
+    return (int)launch_pdl(attn_decode_combine, dim3(heads), dim3(128), st, static_cast<const float*>(ws), splits,
+                           static_cast<__half*>(out));
 }
 
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st) {
-    silu_mul_kernel<<<(n + 255) / 256, 256, 0, st>>>(static_cast<const __half*>(g), static_cast<const __half*>(u),
-                                                     static_cast<__half*>(a), n);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(silu_mul_kernel, dim3((n + 255) / 256), dim3(256), st, static_cast<const __half*>(g),
+                           static_cast<const __half*>(u), static_cast<__half*>(a), n);
 }
 
 }  // namespace abcq

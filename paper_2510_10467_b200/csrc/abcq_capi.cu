@@ -73,6 +73,10 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
+    if (mode >= 3000) {  // CTA partition strategy
+        abcq::g_partition = mode - 3000;
+        return 0;
+    }
     if (mode >= 2000) {  // ring slots issued before the PDL wait
         abcq::g_prefill = mode - 2000;
         return 0;

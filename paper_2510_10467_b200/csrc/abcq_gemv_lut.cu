@@ -10,6 +10,7 @@ int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experi
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
 int g_piece_blocks = 200;
+int g_partition = 0;  // 0: greedy fill with exact piece costs; 1: proportional (abcq_debug_set_mode(3000 + v))
 int g_prefill = 8;  // ring slots issued before the PDL wait (all of them); abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
 
@@ -86,16 +87,57 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     a.n_jobs = n;
     a.total_items = items;
     a.total_units = units;
-    // CTA b owns the items whose first cost unit lies in [b*U/G, (b+1)*U/G)
-    // (computed here once, so the kernel does no 64-bit division)
-    auto first_item = [&](int64_t u) -> int {
-        int j = 0;
-        while (j + 1 < n && a.jobs[j + 1].ubase <= u) ++j;
-        const Job& J = a.jobs[j];
-        const int64_t loc = (u - J.ubase + J.w - 1) / J.w;
-        return J.ibase + (int)(loc < J.items ? loc : J.items);
-    };
-    for (int b = 0; b <= grid; ++b) a.cta_it[b] = first_item((int64_t)b * units / grid);
+    // CTA ranges: greedy fill against a common budget T, with exact piece
+    // accounting -- an item of job j costs p_j blocks, and every (job, slice)
+    // piece a CTA touches costs g_piece_blocks more (its table build and
+    // round switch), however few of its items the CTA takes. The smallest T
+    // that covers all items with `grid` CTAs is found by bisection (host
+    // only; the kernel reads the ranges from its parameters).
+    if (g_partition == 0) {
+        auto fill = [&](int64_t T, bool write) -> bool {  // all items placed within grid CTAs?
+            int j = 0, g = 0;
+            for (int b = 0; b < grid; ++b) {
+                if (write) a.cta_it[b] = g;
+                int64_t cost = 0;
+                while (g < items) {
+                    while (g >= a.jobs[j].ibase + a.jobs[j].items) ++j;
+                    const Job& J = a.jobs[j];
+                    const int loc = g - J.ibase, s = loc / J.NRT;
+                    const int pend = J.ibase + (s + 1) * J.NRT;  // end of this piece
+                    const int64_t start = (int64_t)g_piece_blocks * 64;
+                    const int64_t per = (int64_t)J.p * 64;
+                    if (cost > 0 && cost + start + per > T) break;  // next CTA takes this piece
+                    cost += start;
+                    int64_t take = (T - cost) / per;
+                    if (take < 1) take = 1;
+                    if (take > pend - g) take = pend - g;
+                    cost += take * per;
+                    g += (int)take;
+                    if (cost >= T) break;
+                }
+            }
+            if (write) a.cta_it[grid] = g;
+            return g >= items;
+        };
+        int64_t lo = 1, hi = (int64_t)64 * (units / 64 + 1) + (int64_t)64 * g_piece_blocks * 4 * (items + 1);
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (fill(mid, false)) hi = mid;
+            else lo = mid + 1;
+        }
+        fill(lo, true);
+        a.cta_it[grid] = items;
+    } else {
+        // (partition 1: proportional split of the per-item cost sequence)
+        auto first_item = [&](int64_t u) -> int {
+            int j = 0;
+            while (j + 1 < n && a.jobs[j + 1].ubase <= u) ++j;
+            const Job& J = a.jobs[j];
+            const int64_t loc = (u - J.ubase + J.w - 1) / J.w;
+            return J.ibase + (int)(loc < J.items ? loc : J.items);
+        };
+        for (int b = 0; b <= grid; ++b) a.cta_it[b] = first_item((int64_t)b * units / grid);
+    }
     for (int j = 0; j < n; ++j) {  // CTAs whose range touches job j (arrivals its reduce waits for)
         Job& J = a.jobs[j];
         for (int b = 0; b < grid; ++b)

@@ -52,6 +52,7 @@ extern unsigned long long* g_trace;
 extern int g_dbg_mode;
 extern int g_piece_blocks;
 extern int g_prefill;
+extern int g_partition;
 int num_sms();
 int probe_kernel_image();  // cudaFuncGetAttributes on a packing kernel
 

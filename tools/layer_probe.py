@@ -213,3 +213,10 @@ if "--fit" in sys.argv[0:0] or True:
         print(f"  round 0->1 ({m.sum()} CTAs): warp skew med {np.median(skew):.2f} max {skew.max():.2f} us; "
               f"last warp -> barrier passed med {np.median(bar):.2f}, -> table 1 ready med {np.median(build):.2f} "
               f"max {build.max():.2f} us")
+    # the slowest CTAs' composition (jobs, pieces) and their stream-end times
+    endt = (T[:, 3] - T[:, 3].min()) / 1e3
+    order = np.argsort(-endt)[:6]
+    for b in order:
+        js = sorted({job_of(g) for g in range(cta[b], cta[b + 1])})
+        print(f"    CTA {b:3d}: end +{endt[b]:.2f} us, stream {dur[b]:.2f} us, blocks {F[b,0]:.0f}, pieces {F[b,1]:.0f}, "
+              f"jobs {[(LAYERS[sel[j % len(sel)]][0], jobs[j][2]) for j in js]}")

@@ -30,6 +30,7 @@ namespace abcq {
 constexpr int kGWarps = 8;
 constexpr int kMaxBatch = 16;
 constexpr int kMaxStagePlanes = 4;  // planes staged per item (p_max > 4 loads the rest in rounds)
+constexpr int kMaxSets = 4;         // distinct precisions whose scales are staged with the planes
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
@@ -47,7 +48,17 @@ struct GemmArgs {
     const __half* x;  // (B, cols) fp16
     float* partial;   // [NS][B][NRT*16]
     int p_of[kMaxBatch];
+    int set_of[kMaxBatch];  // request -> index of its precision in pset (-1: not staged)
+    int pset[kMaxSets];     // distinct precisions of the batch (first kMaxSets)
+    int npset;
     int rows, cols, NRT, NS, items, B, pmax;
+};
+
+// dynamic shared memory of the GEMM kernel
+struct GemmSmem {
+    uint4 stage[kGWarps][2][kMaxStagePlanes][32];              // plane blocks, double-buffered
+    uint4 sc[kGWarps][2][kMaxStagePlanes][kMaxSets][8];         // their scales (<= 128 B per set)
+    unsigned char scratch[kGWarps][512];                        // per-warp un-rotated block
 };
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -60,11 +71,14 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 
 template <typename ST, bool ASYM>
 __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArgs a) {
-    __shared__ __align__(16) uint2 nib_tab[16];                    // nibble -> {half2, half2}
-    __shared__ __align__(16) unsigned char scratch[kGWarps][512];  // per-warp un-rotated block
-    // per-warp double buffer of an item's plane blocks, filled with cp.async
-    // (group-tracked, so the next item streams in while this one computes)
-    __shared__ __align__(16) uint4 stage[kGWarps][2][kMaxStagePlanes][32];
+    __shared__ __align__(16) uint2 nib_tab[16];  // nibble -> {half2, half2}
+    // per-warp double buffer of an item's plane blocks and their scales, filled
+    // with cp.async (group-tracked, so the next item streams in while this one
+    // computes)
+    extern __shared__ __align__(16) char gsmem[];
+    GemmSmem& S = *reinterpret_cast<GemmSmem*>(gsmem);
+    auto& stage = S.stage;
+    auto& scratch = S.scratch;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 16) {
@@ -97,9 +111,13 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                 uint32_t v = 0;
                 if (req < B) {
                     const __half* xp = a.x + (int64_t)req * a.cols + k;
-                    const __half lo = k < a.cols ? xp[0] : __float2half(0.f);
-                    const __half hi = k + 1 < a.cols ? xp[1] : __float2half(0.f);
-                    v = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+                    if (k + 1 < a.cols && (a.cols & 1) == 0) {
+                        v = __ldg(reinterpret_cast<const unsigned int*>(xp));  // (k, k+1) as one 32-bit load
+                    } else {
+                        const __half lo = k < a.cols ? xp[0] : __float2half(0.f);
+                        const __half hi = k + 1 < a.cols ? xp[1] : __float2half(0.f);
+                        v = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+                    }
                 }
                 xa[ks][r] = v;
             }
@@ -119,14 +137,22 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
         }
     }
     const int preq0 = g < B ? a.p_of[g] : 0, preq1 = g + 8 < B ? a.p_of[g + 8] : 0;
+    const int set0 = g < B ? a.set_of[g] : -1, set1 = g + 8 < B ? a.set_of[g + 8] : -1;
     const int64_t pstride = (int64_t)B * a.NRT * kTileRows;
 
     // issue the cp.async copies of item rt's planes [i0, i0 + n) into buffer bf
+    constexpr int kScChunks = 32 * (int)sizeof(ST) / 16;  // 16-byte pieces of one plane-item's 32 scales
     auto stage_item = [&](int rt, int bf, int i0) {
         if (rt < a.NRT) {
             const int item = s * a.NRT + rt;
-            for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i)
+            for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i) {
                 cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
+                const int k = lane / kScChunks, c = lane % kScChunks;  // set k, chunk c
+                if (k < a.npset && i < a.pset[k]) {
+                    const ST* al = static_cast<const ST*>(a.alpha[a.pset[k]]) + ((int64_t)i * a.items + item) * 32;
+                    cp_async16(&S.sc[warp][bf][i - i0][k][c], reinterpret_cast<const char*>(al) + 16 * c);
+                }
+            }
         }
         cp_async_commit();
     };
@@ -148,6 +174,7 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
             // un-rotate this plane's 512-byte block into logical row-major bytes:
             // lane (half, r) holds group (2s + half) bytes of row r rotated by r
             const uint4 blk = stage[warp][buf][i % kMaxStagePlanes][lane];
+            const ST* scs = reinterpret_cast<const ST*>(&S.sc[warp][buf][i % kMaxStagePlanes][0][0]);  // [set][32]
             if (i % kMaxStagePlanes == kMaxStagePlanes - 1 && i + 1 < a.pmax) buf ^= 1;  // next round staged in buf^1
             {
                 const int half = lane >> 4, r = lane & 15;
@@ -190,12 +217,16 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                         const int lane_sc = gg * 16 + tr;   // scale lane in the tiled layout
 #pragma unroll
                         for (int rq = 0; rq < 2; ++rq) {
+                            // branch-free: lanes serve different requests (precisions)
                             const int pr = rq ? preq1 : preq0;
-                            if (i < pr) {
+                            const int k = rq ? set1 : set0;
+                            float av = to_f32<ST>(scs[max(k, 0) * (8 * 16 / (int)sizeof(ST)) + lane_sc]);  // staged
+                            if (k < 0 && i < pr) {  // (precisions beyond kMaxSets: global load)
                                 const ST* al = static_cast<const ST*>(a.alpha[pr]);
-                                const float av = to_f32<ST>(al[((int64_t)i * a.items + item) * 32 + lane_sc]);
-                                y[rq][q * 2 + e2] = fmaf(av, c[q][rq * 2 + e2], y[rq][q * 2 + e2]);
+                                av = to_f32<ST>(al[((int64_t)i * a.items + item) * 32 + lane_sc]);
                             }
+                            av = i < pr ? av : 0.f;
+                            y[rq][q * 2 + e2] = fmaf(av, c[q][rq * 2 + e2], y[rq][q * 2 + e2]);
                         }
                     }
                 }
@@ -274,18 +305,29 @@ int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const vo
     a.items = a.NRT * a.NS;
     a.B = B;
     a.pmax = 0;
+    a.npset = 0;
     for (int b = 0; b < B; ++b) {
         a.p_of[b] = p_host[b];
         a.pmax = a.pmax > p_host[b] ? a.pmax : p_host[b];
+        int k = 0;
+        while (k < a.npset && a.pset[k] != p_host[b]) ++k;
+        if (k == a.npset && a.npset < kMaxSets) a.pset[a.npset++] = p_host[b];
+        a.set_of[b] = k < a.npset ? k : -1;
     }
-    const int grid = num_sms() * 4;
-    if (m->scale_dtype == ABCQ_F16) {
-        if (m->asymmetric) gemm_mixedp_kernel<__half, true><<<grid, kGWarps * 32, 0, st>>>(a);
-        else gemm_mixedp_kernel<__half, false><<<grid, kGWarps * 32, 0, st>>>(a);
-    } else {
-        if (m->asymmetric) gemm_mixedp_kernel<float, true><<<grid, kGWarps * 32, 0, st>>>(a);
-        else gemm_mixedp_kernel<float, false><<<grid, kGWarps * 32, 0, st>>>(a);
-    }
+    const int grid = num_sms() * 2;
+    const size_t smem = sizeof(GemmSmem);
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kGWarps * 32, smem, st>>>(a);
+        return cudaGetLastError();
+    };
+    cudaError_t e0;
+    if (m->scale_dtype == ABCQ_F16)
+        e0 = m->asymmetric ? go(gemm_mixedp_kernel<__half, true>) : go(gemm_mixedp_kernel<__half, false>);
+    else
+        e0 = m->asymmetric ? go(gemm_mixedp_kernel<float, true>) : go(gemm_mixedp_kernel<float, false>);
+    if (e0 != cudaSuccess) return (int)e0;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     const int64_t n = (int64_t)B * m->rows;

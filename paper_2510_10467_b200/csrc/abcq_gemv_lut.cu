@@ -1,6 +1,11 @@
 // abcq_gemv_lut.cu -- host launchers of the sm_100a LUT GEMV (kernel:
 // abcq_gemv_batch.cuh): single GEMV (abcq_gemv) and batches of independent
 // GEMVs (abcq_gemv_batch) share one persistent, warp-specialised kernel.
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
 #include "abcq_gemv_batch.cuh"
 
 namespace abcq {
@@ -93,7 +98,32 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     // round switch), however few of its items the CTA takes. The smallest T
     // that covers all items with `grid` CTAs is found by bisection (host
     // only; the kernel reads the ranges from its parameters).
-    if (g_partition == 0) {
+    // the partition depends only on the job shapes and precisions: memoised
+    // (the bisection costs tens of microseconds of host time per call)
+    std::string key;
+    key.reserve(16 + 12 * n);
+    auto put = [&](int v) { key.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
+    put(grid);
+    put(g_partition);
+    put(g_piece_blocks);
+    for (int j = 0; j < n; ++j) {
+        put(a.jobs[j].rows);
+        put(a.jobs[j].cols);
+        put(a.jobs[j].p);
+    }
+    static std::mutex memo_mu;
+    static std::unordered_map<std::string, std::vector<int>> memo;
+    bool have = false;
+    {
+        std::lock_guard<std::mutex> lk(memo_mu);
+        auto it = memo.find(key);
+        if (it != memo.end()) {
+            for (int b = 0; b <= grid; ++b) a.cta_it[b] = it->second[b];
+            have = true;
+        }
+    }
+    if (have) {
+    } else if (g_partition == 0) {
         auto fill = [&](int64_t T, bool write) -> bool {  // all items placed within grid CTAs?
             int j = 0, g = 0;
             for (int b = 0; b < grid; ++b) {
@@ -137,6 +167,11 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             return J.ibase + (int)(loc < J.items ? loc : J.items);
         };
         for (int b = 0; b <= grid; ++b) a.cta_it[b] = first_item((int64_t)b * units / grid);
+    }
+    if (!have) {
+        std::lock_guard<std::mutex> lk(memo_mu);
+        if (memo.size() > 4096) memo.clear();
+        memo.emplace(key, std::vector<int>(a.cta_it, a.cta_it + grid + 1));
     }
     for (int j = 0; j < n; ++j) {  // CTAs whose range touches job j (arrivals its reduce waits for)
         Job& J = a.jobs[j];

@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         enter_round(k, k.rend);
     };
     const uint64_t pol = l2_evict_first_policy();
+    const uint64_t pol_keep = l2_evict_last_policy();
     // issue the TMA copies of the cursor's element into slot s (lane 0 only)
     auto issue = [&](const Cur& k, int s) {
         const int cnt = min(kK, k.hi - k.c);
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 #pragma unroll
                     for (int q = 0; q < kK; ++q)
                         if (q < cnt && lane < 16)
-                            __stcg(part + (int64_t)(c + q - tile0) * NS * kTileRows + lane, outv[q]);
+                            st_f32_hint(part + (int64_t)(c + q - tile0) * NS * kTileRows + lane, outv[q], pol_keep);
                 }
             }
         };

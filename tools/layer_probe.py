@@ -18,7 +18,8 @@ from paper_2510_10467_b200 import _lib  # noqa: E402
 from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
-          ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+          ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336),
+          ("gate70", 28672, 8192), ("down70", 8192, 28672)]  # (7, 8: 70B shapes)
 NAMES = ["start", "-", "tab0", "streamed", "r0first", "r0last"]
 
 ap = argparse.ArgumentParser()

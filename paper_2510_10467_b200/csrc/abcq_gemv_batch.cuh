@@ -48,6 +48,7 @@ template <int NJ>
 struct KArgs {
     Job jobs[NJ];
     int cta_it[kMaxGrid + 1];  // CTA b owns batch items [cta_it[b], cta_it[b+1]) (host-computed)
+    int main_ctas;             // GEMV CTAs; CTAs beyond them complete the split-K sums
     int n_jobs;
     int total_items;
     int64_t total_units;
@@ -59,6 +60,7 @@ struct KArgs {
 struct BatchArgs {
     Job jobs[kMaxJobs];
     int cta_it[kMaxGrid + 1];
+    int main_ctas;
     int n_jobs;
     int total_items;
     int64_t total_units;
@@ -177,6 +179,69 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
     }
 }
 
+constexpr int kReduceRows = 512;  // rows per block of the standalone reduce kernel (1024 threads)
+
+// one reduce block: rows [blk*RPB, (blk+1)*RPB) of the blk-th block's job
+// (blocks laid out job by job), two threads per row (blockDim.x == 2*RPB)
+template <int NJ, typename YT, int RPB>
+__device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
+    constexpr int rpb = RPB;  // rows per block (two threads per row)
+    int j = 0, nbj = 0;
+    for (; j < a.n_jobs; ++j) {
+        const Job& J = a.jobs[j];
+        if (J.NS <= 1) continue;
+        nbj = (J.rows + rpb - 1) / rpb;
+        if (blk < nbj) break;
+        blk -= nbj;
+    }
+    if (j >= a.n_jobs) return;
+    const Job& J = a.jobs[j];
+    // wait for this job's CTA arrivals only (acquire), so the reduction
+    // overlaps the GEMV CTAs still streaming other jobs
+    if (threadIdx.x == 0) {
+        uint32_t seen;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
+            if (seen >= (uint32_t)J.ncta) break;
+            __nanosleep(128);
+        }
+        if (a.trace) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
+    }
+    __syncthreads();
+    const int hh = threadIdx.x & 1;  // chains 2hh, 2hh+1
+    const int row = blk * rpb + (threadIdx.x >> 1);
+    const float* pp = partial_row(J, row < J.rows ? row : 0);
+    const int nblk = (J.NS + 15) / 16;  // 16-slice blocks (the padding unit)
+    float c[2] = {0.f, 0.f};
+    for (int b0 = 0; b0 < nblk; b0 += 2) {  // up to 16 loads in flight
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {  // k: block b0 + k/8, term (k%8)/2 of chain 2hh + k%2
+            const int bb = b0 + (k >> 3);
+            const int s = bb * 16 + ((k & 7) >> 1) * 4 + 2 * hh + (k & 1);
+            v[k] = (bb < nblk && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (b0 + (k >> 3) < nblk) c[k & 1] += v[k];
+    }
+    const float mine = c[0] + c[1];  // hh=0: c0+c1, hh=1: c2+c3
+    const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+    if (hh == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.trace) {  // profiling: last block end, per job
+            const unsigned long long t = globaltimer();
+            atomicMax(&a.trace[148 * 8 + 2], t);
+            if (j < 32) atomicMax(&a.trace[149 * 8 + j], t);
+        }
+        if (atomicAdd(J.reduced, 1u) == (uint32_t)(nbj - 1)) {  // last block of job j: recycle
+            *J.arrive = 0u;
+            *J.reduced = 0u;
+        }
+    }
+}
+
 // profiling stamps (abcq_debug_set_trace): per CTA, slot k = max over the
 // calling warps of %globaltimer. 0 start, 1 after the PDL wait, 2 first table
 // ready, 3 streams done, 4 / 5 first / last warp done with round 0, 6 =
@@ -186,8 +251,20 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
     } while (0)
 
-template <int NJ, typename XT, typename YT, typename ST, bool ASYM>
+template <int NJ, typename XT, typename YT, typename ST, bool ASYM, bool FUSED>
 __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_constant__ KArgs<NJ> a) {
+    if constexpr (FUSED) {
+        if ((int)blockIdx.x >= a.main_ctas) {
+            // trailing CTAs: split-K completion (they get SMs as GEMV CTAs
+            // retire) -- for batches whose reduce fits one wave; larger ones
+            // use the separate kernel (a trailing CTA needs a whole SM, and
+            // the role's code in the kernel costs the streams ~7%)
+            pdl_launch_dependents();
+            pdl_wait();  // (y may still be read by the previous kernel)
+            reduce_rows<NJ, YT, kBThreads / 2>(a, blockIdx.x - a.main_ctas);
+            return;
+        }
+    }
     using SG = SlotGeom<ST, ASYM>;
     constexpr int R = SG::kRing;
     extern __shared__ __align__(1024) char smem[];
@@ -545,71 +622,14 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 // chains 2h and 2h+1 of the split-K order (chain m = slices s = m mod 4,
 // ascending, zero-padded to whole 16-slice blocks), up to 16 loads in flight;
 // then (c0 + c1) + (c2 + c3) -- independent of the batch composition.
-constexpr int kReduceRows = 512;  // two threads per row, 1024-thread blocks: a 21-GEMV batch is one wave
+// Standalone split-K completion kernel (PDL-chained; debug mode 22): the
+// default folds these blocks into the GEMV grid itself (trailing CTAs,
+// gemv_batch_kernel) -- one launch per batch, no kernel boundary.
 template <int NJ, typename YT>
-__global__ void __launch_bounds__(2 * kReduceRows) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
+__global__ void __launch_bounds__(2 * kReduceRows, 2) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {  // 2 blocks/SM
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
     pdl_launch_dependents();
-    int blk = blockIdx.x, j = 0, nbj = 0;
-    for (; j < a.n_jobs; ++j) {
-        const Job& J = a.jobs[j];
-        if (J.NS <= 1) continue;
-        nbj = (J.rows + kReduceRows - 1) / kReduceRows;
-        if (blk < nbj) break;
-        blk -= nbj;
-    }
-    if (j >= a.n_jobs) {
-        pdl_wait();
-        return;
-    }
-    const Job& J = a.jobs[j];
-    // no griddepcontrol.wait up front: wait for this job's CTA arrivals only
-    // (acquire), so the reduction overlaps the GEMV kernel's straggler CTAs.
-    // (The GEMV kernel waited for all earlier work before it let this grid
-    // launch; this grid waits for the GEMV grid before it exits, so the next
-    // kernel sees both complete.)
-    if (threadIdx.x == 0) {
-        uint32_t seen;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
-            if (seen >= (uint32_t)J.ncta) break;
-            __nanosleep(128);
-        }
-        if (a.trace) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
-    }
-    __syncthreads();
-    const int hh = threadIdx.x & 1;  // chains 2hh, 2hh+1
-    const int row = blk * kReduceRows + (threadIdx.x >> 1);
-    const float* pp = partial_row(J, row < J.rows ? row : 0);
-    const int nblk = (J.NS + 15) / 16;  // 16-slice blocks (the padding unit)
-    float c[2] = {0.f, 0.f};
-    for (int b0 = 0; b0 < nblk; b0 += 2) {  // up to 16 loads in flight
-        float v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {  // k: block b0 + k/8, term (k%8)/2 of chain 2hh + k%2
-            const int bb = b0 + (k >> 3);
-            const int s = bb * 16 + ((k & 7) >> 1) * 4 + 2 * hh + (k & 1);
-            v[k] = (bb < nblk && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (b0 + (k >> 3) < nblk) c[k & 1] += v[k];
-    }
-    const float mine = c[0] + c[1];  // hh=0: c0+c1, hh=1: c2+c3
-    const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-    if (hh == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (a.trace) {  // profiling: last block end, per job
-            const unsigned long long t = globaltimer();
-            atomicMax(&a.trace[148 * 8 + 2], t);
-            if (j < 32) atomicMax(&a.trace[149 * 8 + j], t);
-        }
-        if (atomicAdd(J.reduced, 1u) == (uint32_t)(nbj - 1)) {  // last block of job j: recycle
-            *J.arrive = 0u;
-            *J.reduced = 0u;
-        }
-    }
+    reduce_rows<NJ, YT, kReduceRows>(a, blockIdx.x);
     pdl_wait();  // the GEMV grid (y of unsplit jobs) completes before this grid does
 }
 
@@ -618,13 +638,20 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     KArgs<NJ> a;
     for (int j = 0; j < ba.n_jobs; ++j) a.jobs[j] = ba.jobs[j];
     a.n_jobs = ba.n_jobs;
+    a.main_ctas = grid;
     for (int i = 0; i <= grid && i <= kMaxGrid; ++i) a.cta_it[i] = ba.cta_it[i];
     a.total_items = ba.total_items;
     a.total_units = ba.total_units;
     a.prefill = ba.prefill;
     a.dbg = ba.dbg;
     a.trace = ba.trace;
-    auto kern = gemv_batch_kernel<NJ, XT, YT, ST, ASYM>;
+    int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/2) per job)
+    for (int j = 0; j < ba.n_jobs; ++j)
+        if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kBThreads / 2 - 1) / (kBThreads / 2);
+    constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
+    const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
+    auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>
+                      : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>;
     constexpr int smem = SlotGeom<ST, ASYM>::kSmem;
     static_assert(smem <= 227 * 1024, "shared memory budget");
     static_assert(SlotGeom<ST, ASYM>::kRing >= 2, "ring too shallow");
@@ -632,19 +659,28 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     cudaGetDevice(&dev);
     static bool attr_set[64] = {};  // per instantiation and device
     if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return (int)e;
         // the reduce kernel keeps the GEMV's shared-memory carveout: an SM that
         // ran it must not be reconfigured before the next GEMV CTA can start
         e = cudaFuncSetAttribute(batch_reduce_kernel<NJ, YT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return (int)e;
         attr_set[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    const bool separate = !fused;
+    cfg.gridDim = dim3(grid + (separate ? 0 : rblocks));
     cfg.blockDim = dim3(kBThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -654,8 +690,8 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e != cudaSuccess) return (int)e;
-    int nblocks = 0;  // one reduce launch for every split job of the batch
+    if (e != cudaSuccess || !separate) return (int)e;
+    int nblocks = 0;  // one separate reduce launch
     for (int j = 0; j < a.n_jobs; ++j)
         if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
     if (nblocks == 0) return 0;

@@ -179,7 +179,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             if (a.cta_it[b] < J.ibase + J.items && a.cta_it[b + 1] > J.ibase && a.cta_it[b] < a.cta_it[b + 1]) ++J.ncta;
     }
     a.prefill = g_prefill;
-    a.dbg = g_dbg_mode == 1 ? 1 : 0;
+    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22) ? g_dbg_mode : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
     const abcq_model_t* m = models[0];

@@ -203,7 +203,7 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         for (;;) {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
             if (seen >= (uint32_t)J.ncta) break;
-            __nanosleep(128);
+            __nanosleep(32);
         }
         if (a.trace) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
     }
@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     // publish this CTA's split-K partials: one release per CTA, one arrival per
     // split job it touched -- the reduce kernel starts on a job as soon as all
     // of its CTAs arrived, while stragglers are still streaming other jobs
+    // (per-warp release arrivals were measured slower: one hot counter)
     __syncthreads();
     if (tid == 0 && it0 < it1) {
         __threadfence();

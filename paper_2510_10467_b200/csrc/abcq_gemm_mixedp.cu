@@ -14,12 +14,13 @@
 // progressive.py:32-79).
 //
 // Mapping: Y^T (requests x rows) = X (requests x K) . W^T. A = X fragment
-// (16 requests x 16 k, fp16, kept in registers for the warp's slice); B = the
+// (16 requests x 16 k, fp16; the CTA's slice of X is staged in shared memory
+// once and read with ldmatrix, one 128-column group at a time); B = the
 // sign bits of 8 weight rows, expanded to +-1 fp16 through a 16-entry nibble
 // table in shared memory (a lane's B fragment is one nibble per row and
 // k-step); C = 16 requests x 8 rows, reset per 128-column group, scaled by
 // alpha^(p_b) and accumulated. Weight blocks (tiled layout, rotated bytes) are
-// un-rotated through a per-warp shared-memory scratch.
+// read straight from the staging buffer and un-rotated in registers.
 // This is a dense contraction (2*B flops per weight bit), hence tensor cores;
 // the batch-1 path is the LUT kernel.
 #include "abcq_common.cuh"
@@ -51,34 +52,80 @@ struct GemmArgs {
     int set_of[kMaxBatch];  // request -> index of its precision in pset (-1: not staged)
     int pset[kMaxSets];     // distinct precisions of the batch (first kMaxSets)
     int npset;
+    int overflow;           // some request's precision is not among pset (its scales are read from global)
     int rows, cols, NRT, NS, items, B, pmax;
+    int cps;  // CTAs per slice (each takes every cps-th group of kGWarps row tiles)
 };
 
 // dynamic shared memory of the GEMM kernel
+constexpr int kXPitch = 256 + 8;  // halves per staged X row: 528 B, ldmatrix rows hit distinct banks
 struct GemmSmem {
     uint4 stage[kGWarps][2][kMaxStagePlanes][32];              // plane blocks, double-buffered
     uint4 sc[kGWarps][2][kMaxStagePlanes][kMaxSets][8];         // their scales (<= 128 B per set)
-    unsigned char scratch[kGWarps][512];                        // per-warp un-rotated block
+    __align__(16) __half xs[kMaxBatch][kXPitch];                // the CTA's X slice (16 requests x 256 k)
 };
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* smem) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"((uint32_t)__cvta_generic_to_shared(smem)));
+}
+
+// One 16-byte lane chunk of a tiled block holds a row's group bytes rotated by
+// the row index r (stored byte j = logical byte (j + r) & 15); undo it in
+// registers: logical = stored rotated left by r bytes. K2 = bit 3 of r (a
+// compile-time word swap), k1 = bit 2, sh = 8 * (r & 3).
+template <bool K2>
+__device__ __forceinline__ void unrotate16(const uint4 v, bool k1, int sh, uint32_t (&o)[4]) {
+    uint32_t w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
+    if (K2) {  // R[m] = S[m - 2]
+        uint32_t t0 = w0, t1 = w1;
+        w0 = w2; w1 = w3; w2 = t0; w3 = t1;
+    }
+    if (k1) {  // R[m] = S[m - 1]
+        uint32_t t = w3;
+        w3 = w2; w2 = w1; w1 = w0; w0 = t;
+    }
+    o[0] = __funnelshift_l(w3, w0, sh);
+    o[1] = __funnelshift_l(w0, w1, sh);
+    o[2] = __funnelshift_l(w1, w2, sh);
+    o[3] = __funnelshift_l(w2, w3, sh);
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+template <typename ST>
+__device__ __forceinline__ float2 ld_scale2(const ST* p);
+template <>
+__device__ __forceinline__ float2 ld_scale2<__half>(const __half* p) {
+    return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
+template <>
+__device__ __forceinline__ float2 ld_scale2<float>(const float* p) {
+    return *reinterpret_cast<const float2*>(p);
+}
+
 template <typename ST, bool ASYM>
 __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArgs a) {
-    __shared__ __align__(16) uint2 nib_tab[16];  // nibble -> {half2, half2}
+    __shared__ __align__(128) uint2 nib_tab[16];  // nibble -> {half2, half2}; 128-aligned: address = base | 8*nibble
     // per-warp double buffer of an item's plane blocks and their scales, filled
     // with cp.async (group-tracked, so the next item streams in while this one
-    // computes)
+    // computes); the CTA's X slice, read as A fragments with ldmatrix
     extern __shared__ __align__(16) char gsmem[];
     GemmSmem& S = *reinterpret_cast<GemmSmem*>(gsmem);
     auto& stage = S.stage;
-    auto& scratch = S.scratch;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 16) {
@@ -86,181 +133,194 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
         auto h = [](int bit) -> uint32_t { return bit ? 0x3C00u : 0xBC00u; };  // +1 / -1 in fp16
         nib_tab[n] = make_uint2(h(n & 1) | (h((n >> 1) & 1) << 16), h((n >> 2) & 1) | (h((n >> 3) & 1) << 16));
     }
-    __syncthreads();
 
     const int g = lane >> 2, t = lane & 3;
-    const int gw = blockIdx.x * kGWarps + warp, W = gridDim.x * kGWarps;
-    // this warp's slice and row tiles: warps cycle over slices first
-    const int s = gw % a.NS;
-    const int wps = W / a.NS + (gw % a.NS < W % a.NS ? 1 : 0);  // warps on slice s
-    const int widx = gw / a.NS;
-    if (widx >= a.NRT) return;
     const int B = a.B;
+    const int preq0 = g < B ? a.p_of[g] : 0, preq1 = g + 8 < B ? a.p_of[g + 8] : 0;
+    const int set0 = g < B ? a.set_of[g] : -1, set1 = g + 8 < B ? a.set_of[g + 8] : -1;
+    // element offsets of the lane's two requests' staged scale sets
+    const int soff0 = max(set0, 0) * (8 * 16 / (int)sizeof(ST)), soff1 = max(set1, 0) * (8 * 16 / (int)sizeof(ST));
+    const int64_t pstride = (int64_t)B * a.NRT * kTileRows;
+    const bool xvec = (a.cols & 7) == 0 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+    // this lane's ldmatrix row address inside the X slice (matrix lane>>3: rows +8, k +8)
+    const int xrow = (lane & 7) + ((lane >> 3) & 1) * 8, xcol = (lane >> 4) * 8;
+    const int tstride = a.cps * kGWarps;  // tiles per slice step of a warp
+    const uint32_t nib_base = (uint32_t)__cvta_generic_to_shared(nib_tab);
+    const bool rk1 = (g >> 2) & 1;  // bit 2 of the lane's rows g, g+8 (their rotations)
+    const int rsh = 8 * (g & 3);
 
-    // A fragments (X) of the whole 256-column slice: 16 k-steps x 4 regs
-    uint32_t xa[16][4];
-    float gxs[2][2];  // per group: sum of x over the group for requests g, g+8 (asymmetric)
-    {
+    // units = (slice, chunk of the slice's row tiles); a CTA's warps share the slice
+    for (int u = blockIdx.x; u < a.NS * a.cps; u += gridDim.x) {
+        const int s = u % a.NS, chunk = u / a.NS;
         const int k0 = s * kSliceCols;
+        __syncthreads();  // the previous unit's X reads are done (and nib_tab is written)
+        // X slice -> shared, k permuted inside each 16-column k-step so that the four
+        // k a lane feeds the MMA (2t, 2t+1, 2t+8, 2t+9) are weight bits 4t..4t+3, one
+        // contiguous nibble: MMA k = m holds column 4*((m & 7) >> 1) + 2*(m >> 3) + (m & 1),
+        // i.e. the low 8 MMA columns take the column pairs (0,1),(4,5),(8,9),(12,13)
+        // and the high 8 take (2,3),(6,7),(10,11),(14,15).
+        for (int cidx = threadIdx.x; cidx < kMaxBatch * 16; cidx += blockDim.x) {
+            const int req = cidx >> 4, ks = cidx & 15, kc = ks * 16, k = k0 + kc;
+            uint32_t e[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // column pairs of the k-step
+            if (req < B) {
+                const __half* xp = a.x + (int64_t)req * a.cols + k;
+                if (xvec && k + 16 <= a.cols) {
+                    const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(xp));
+                    const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(xp) + 1);
+                    e[0] = v0.x; e[1] = v0.y; e[2] = v0.z; e[3] = v0.w;
+                    e[4] = v1.x; e[5] = v1.y; e[6] = v1.z; e[7] = v1.w;
+                } else {
 #pragma unroll
-        for (int ks = 0; ks < 16; ++ks) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int req = g + ((r & 1) ? 8 : 0);
-                const int k = k0 + ks * 16 + 2 * t + ((r & 2) ? 8 : 0);
-                uint32_t v = 0;
-                if (req < B) {
-                    const __half* xp = a.x + (int64_t)req * a.cols + k;
-                    if (k + 1 < a.cols && (a.cols & 1) == 0) {
-                        v = __ldg(reinterpret_cast<const unsigned int*>(xp));  // (k, k+1) as one 32-bit load
-                    } else {
-                        const __half lo = k < a.cols ? xp[0] : __float2half(0.f);
-                        const __half hi = k + 1 < a.cols ? xp[1] : __float2half(0.f);
-                        v = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
-                    }
+                    for (int j = 0; j < 16; ++j)
+                        if (k + j < a.cols) e[j >> 1] |= (uint32_t)__half_as_ushort(xp[j]) << (16 * (j & 1));
                 }
-                xa[ks][r] = v;
             }
+            *reinterpret_cast<uint4*>(&S.xs[req][kc]) = make_uint4(e[0], e[2], e[4], e[6]);
+            *reinterpret_cast<uint4*>(&S.xs[req][kc + 8]) = make_uint4(e[1], e[3], e[5], e[7]);
         }
+        __syncthreads();
+        float gxs[2][2];  // per group: sum of x over the group for requests g, g+8 (asymmetric)
         if (ASYM) {
 #pragma unroll
             for (int gg = 0; gg < 2; ++gg)
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const int req = g + 8 * q;
-                    float sum = 0.f;
-                    if (req < B)
-                        for (int k = k0 + gg * 128; k < min(k0 + gg * 128 + 128, a.cols); ++k)
-                            sum += __half2float(a.x[(int64_t)req * a.cols + k]);
+                    float sum = 0.f;  // lanes t split the group's 128 columns, fixed order
+                    for (int k = 0; k < 32; ++k) sum += __half2float(S.xs[g + 8 * q][gg * 128 + t * 32 + k]);
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
                     gxs[gg][q] = sum;
                 }
         }
-    }
-    const int preq0 = g < B ? a.p_of[g] : 0, preq1 = g + 8 < B ? a.p_of[g + 8] : 0;
-    const int set0 = g < B ? a.set_of[g] : -1, set1 = g + 8 < B ? a.set_of[g + 8] : -1;
-    const int64_t pstride = (int64_t)B * a.NRT * kTileRows;
 
-    // issue the cp.async copies of item rt's planes [i0, i0 + n) into buffer bf
-    constexpr int kScChunks = 32 * (int)sizeof(ST) / 16;  // 16-byte pieces of one plane-item's 32 scales
-    auto stage_item = [&](int rt, int bf, int i0) {
-        if (rt < a.NRT) {
-            const int item = s * a.NRT + rt;
-            for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i) {
-                cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
-                const int k = lane / kScChunks, c = lane % kScChunks;  // set k, chunk c
-                if (k < a.npset && i < a.pset[k]) {
-                    const ST* al = static_cast<const ST*>(a.alpha[a.pset[k]]) + ((int64_t)i * a.items + item) * 32;
-                    cp_async16(&S.sc[warp][bf][i - i0][k][c], reinterpret_cast<const char*>(al) + 16 * c);
-                }
-            }
-        }
-        cp_async_commit();
-    };
-    int buf = 0;
-    stage_item(widx, 0, 0);
-    for (int rt = widx; rt < a.NRT; rt += wps, buf ^= 1) {
-        const int item = s * a.NRT + rt;
-        // accumulators: requests {g, g+8} x tile rows {2t, 2t+1, 8+2t, 8+2t+1}
-        float y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        for (int i = 0; i < a.pmax; ++i) {
-            if (i % kMaxStagePlanes == 0) {
-                // planes [i, i+4) of this item are (being) staged in `buf`: prefetch the
-                // next round (more planes of this item, or the next item) into buf^1
-                if (i + kMaxStagePlanes < a.pmax) stage_item(rt, buf ^ 1, i + kMaxStagePlanes);
-                else stage_item(rt + wps, buf ^ 1, 0);
-                cp_async_wait<1>();
-                __syncwarp();
-            }
-            // un-rotate this plane's 512-byte block into logical row-major bytes:
-            // lane (half, r) holds group (2s + half) bytes of row r rotated by r
-            const uint4 blk = stage[warp][buf][i % kMaxStagePlanes][lane];
-            const ST* scs = reinterpret_cast<const ST*>(&S.sc[warp][buf][i % kMaxStagePlanes][0][0]);  // [set][32]
-            if (i % kMaxStagePlanes == kMaxStagePlanes - 1 && i + 1 < a.pmax) buf ^= 1;  // next round staged in buf^1
-            {
-                const int half = lane >> 4, r = lane & 15;
-                const uint32_t wv[4] = {blk.x, blk.y, blk.z, blk.w};
-#pragma unroll
-                for (int j = 0; j < 16; ++j)  // stored byte j = logical byte (j + r) & 15
-                    scratch[warp][r * 32 + half * 16 + ((j + r) & 15)] = (unsigned char)(wv[j >> 2] >> (8 * (j & 3)));
-            }
-            __syncwarp();
-            // rows g and g+8 of the tile: 32 logical bytes each
-            uint32_t rowb[2][8];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const uint4 lo = *reinterpret_cast<const uint4*>(&scratch[warp][(g + 8 * q) * 32]);
-                const uint4 hi = *reinterpret_cast<const uint4*>(&scratch[warp][(g + 8 * q) * 32 + 16]);
-                rowb[q][0] = lo.x; rowb[q][1] = lo.y; rowb[q][2] = lo.z; rowb[q][3] = lo.w;
-                rowb[q][4] = hi.x; rowb[q][5] = hi.y; rowb[q][6] = hi.z; rowb[q][7] = hi.w;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int gg = 0; gg < 2; ++gg) {  // two 128-column groups of the slice
-                float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int ks = gg * 8 + kk;
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {  // q: weight rows g (0-7 tile) / g+8 (8-15 tile)
-                        const uint32_t hw = rowb[q][ks >> 1] >> (16 * (ks & 1));  // bytes 2ks, 2ks+1
-                        const uint32_t nib = ((hw >> (2 * t)) & 3u) | ((hw >> (8 + 2 * t - 2)) & 0xCu);
-                        const uint2 bf = nib_tab[nib];
-                        mma16816(c[q], xa[ks], bf.x, bf.y);
-                    }
-                }
-                // scale: C[q] holds requests {g, g+8} x rows {q*8 + 2t, q*8 + 2t + 1}
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-#pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) {
-                        const int tr = q * 8 + 2 * t + e2;  // tile row
-                        const int lane_sc = gg * 16 + tr;   // scale lane in the tiled layout
-#pragma unroll
-                        for (int rq = 0; rq < 2; ++rq) {
-                            // branch-free: lanes serve different requests (precisions)
-                            const int pr = rq ? preq1 : preq0;
-                            const int k = rq ? set1 : set0;
-                            float av = to_f32<ST>(scs[max(k, 0) * (8 * 16 / (int)sizeof(ST)) + lane_sc]);  // staged
-                            if (k < 0 && i < pr) {  // (precisions beyond kMaxSets: global load)
-                                const ST* al = static_cast<const ST*>(a.alpha[pr]);
-                                av = to_f32<ST>(al[((int64_t)i * a.items + item) * 32 + lane_sc]);
-                            }
-                            av = i < pr ? av : 0.f;
-                            y[rq][q * 2 + e2] = fmaf(av, c[q][rq * 2 + e2], y[rq][q * 2 + e2]);
+        // issue the cp.async copies of tile rt's planes [i0, i0 + n) into buffer bf
+        constexpr int kScChunks = 32 * (int)sizeof(ST) / 16;  // 16-byte pieces of one plane-item's 32 scales
+        auto stage_item = [&](int rt, int bf, int i0) {
+            if (rt < a.NRT) {
+                const int item = s * a.NRT + rt;
+                for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i) {
+                    cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
+                    const int k = lane / kScChunks, c = lane % kScChunks;  // set k, chunk c
+                    if (k < a.npset) {
+                        if (i < a.pset[k]) {
+                            const ST* al = static_cast<const ST*>(a.alpha[a.pset[k]]) + ((int64_t)i * a.items + item) * 32;
+                            cp_async16(&S.sc[warp][bf][i - i0][k][c], reinterpret_cast<const char*>(al) + 16 * c);
+                        } else {  // plane i is beyond this set's precision: scale 0
+                            S.sc[warp][bf][i - i0][k][c] = make_uint4(0u, 0u, 0u, 0u);
                         }
                     }
                 }
-                if (ASYM && i == 0) {
+            }
+            cp_async_commit();
+        };
+        int buf = 0;
+        const int rt0 = chunk * kGWarps + warp;
+        stage_item(rt0, 0, 0);
+        for (int rt = rt0; rt < a.NRT; rt += tstride) {
+            const int item = s * a.NRT + rt;
+            // accumulators: requests {g, g+8} x tile rows {2t, 2t+1, 8+2t, 8+2t+1}
+            float y[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            for (int i0 = 0; i0 < a.pmax; i0 += kMaxStagePlanes, buf ^= 1) {
+                // planes [i0, i0+4) of this tile are (being) staged in `buf`: prefetch the
+                // next round (more planes of this tile, or the next tile) into buf^1
+                if (i0 + kMaxStagePlanes < a.pmax) stage_item(rt, buf ^ 1, i0 + kMaxStagePlanes);
+                else stage_item(rt + tstride, buf ^ 1, 0);
+                cp_async_wait<1>();
+                __syncwarp();
+                const int np = min(kMaxStagePlanes, a.pmax - i0);
+#pragma unroll
+                for (int gg = 0; gg < 2; ++gg) {  // two 128-column groups of the slice
+                    uint32_t xa[8][4];            // A fragments of this group's 8 k-steps
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) ldmatrix_x4(xa[kk], &S.xs[xrow][gg * 128 + kk * 16 + xcol]);
+                    for (int ii = 0; ii < np; ++ii) {
+                        const int i = i0 + ii;
+                        // rows g and g+8 of the tile: their 16 group bytes (lane chunk gg*16 + row)
+                        uint32_t rowb[2][4];
+                        unrotate16<false>(stage[warp][buf][ii][gg * 16 + g], rk1, rsh, rowb[0]);
+                        unrotate16<true>(stage[warp][buf][ii][gg * 16 + g + 8], rk1, rsh, rowb[1]);
+                        const ST* scs = reinterpret_cast<const ST*>(&S.sc[warp][buf][ii][0][0]);  // [set][32]
+                        float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {  // q: weight rows g (0-7 tile) / g+8 (8-15 tile)
+                                // weight bits 4t..4t+3 of k-step kk (see the X permutation), as
+                                // the byte offset 8 * nibble of its table entry
+                                const uint32_t w = rowb[q][kk >> 1];
+                                const uint32_t off = (kk & 1) ? (w >> (13 + 4 * t)) & 0x78u : ((w << 3) >> (4 * t)) & 0x78u;
+                                const uint2 bf = lds64(nib_base | off);
+                                mma16816(c[q], xa[kk], bf.x, bf.y);
+                            }
+                        }
+                        // scale: C[q] holds requests {g, g+8} x rows {q*8 + 2t, q*8 + 2t + 1};
+                        // staged sets are zero beyond their precision, so no masking
+                        if (!a.overflow) {
+#pragma unroll
+                            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                                for (int rq = 0; rq < 2; ++rq) {
+                                    const float2 av = ld_scale2<ST>(scs + (rq ? soff1 : soff0) + gg * 16 + q * 8 + 2 * t);
+                                    y[rq][q * 2] = fmaf(av.x, c[q][rq * 2], y[rq][q * 2]);
+                                    y[rq][q * 2 + 1] = fmaf(av.y, c[q][rq * 2 + 1], y[rq][q * 2 + 1]);
+                                }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+#pragma unroll
+                                for (int e2 = 0; e2 < 2; ++e2) {
+                                    const int lane_sc = gg * 16 + q * 8 + 2 * t + e2;  // scale lane in the tiled layout
+#pragma unroll
+                                    for (int rq = 0; rq < 2; ++rq) {
+                                        const int pr = rq ? preq1 : preq0;
+                                        const int k = rq ? set1 : set0;
+                                        float av = to_f32<ST>(scs[(rq ? soff1 : soff0) + lane_sc]);
+                                        if (k < 0 && i < pr) {  // precisions beyond kMaxSets: global load
+                                            const ST* al = static_cast<const ST*>(a.alpha[pr]);
+                                            av = to_f32<ST>(al[((int64_t)i * a.items + item) * 32 + lane_sc]);
+                                        }
+                                        av = i < pr ? av : 0.f;
+                                        y[rq][q * 2 + e2] = fmaf(av, c[q][rq * 2 + e2], y[rq][q * 2 + e2]);
+                                    }
+                                }
+                            }
+                        }
+                        if (ASYM && i == 0) {
+#pragma unroll
+                            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                                for (int e2 = 0; e2 < 2; ++e2)
+#pragma unroll
+                                    for (int rq = 0; rq < 2; ++rq) {
+                                        const int pr = rq ? preq1 : preq0;
+                                        if (pr > 0) {
+                                            const ST* of = static_cast<const ST*>(a.offset[pr]);
+                                            const float zv =
+                                                to_f32<ST>(of[(int64_t)item * 32 + gg * 16 + q * 8 + 2 * t + e2]);
+                                            y[rq][q * 2 + e2] = fmaf(zv, gxs[gg][rq], y[rq][q * 2 + e2]);
+                                        }
+                                    }
+                        }
+                    }
+                }
+                __syncwarp();  // all lanes are done with `buf` before it is refilled
+            }
+            // partial[s][req][row]
+#pragma unroll
+            for (int rq = 0; rq < 2; ++rq) {
+                const int req = g + 8 * rq;
+                if (req < B) {
 #pragma unroll
                     for (int q = 0; q < 2; ++q)
 #pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2)
-#pragma unroll
-                            for (int rq = 0; rq < 2; ++rq) {
-                                const int pr = rq ? preq1 : preq0;
-                                if (pr > 0) {
-                                    const ST* of = static_cast<const ST*>(a.offset[pr]);
-                                    const float zv = to_f32<ST>(of[(int64_t)item * 32 + gg * 16 + q * 8 + 2 * t + e2]);
-                                    y[rq][q * 2 + e2] = fmaf(zv, gxs[gg][rq], y[rq][q * 2 + e2]);
-                                }
-                            }
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            const int row = rt * kTileRows + q * 8 + 2 * t + e2;
+                            a.partial[s * pstride + (int64_t)req * a.NRT * kTileRows + row] = y[rq][q * 2 + e2];
+                        }
                 }
             }
         }
-        // partial[s][req][row]
-#pragma unroll
-        for (int rq = 0; rq < 2; ++rq) {
-            const int req = g + 8 * rq;
-            if (req < B) {
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-#pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) {
-                        const int row = rt * kTileRows + q * 8 + 2 * t + e2;
-                        a.partial[s * pstride + (int64_t)req * a.NRT * kTileRows + row] = y[rq][q * 2 + e2];
-                    }
-            }
-        }
+        cp_async_wait<0>();
     }
 }
 
@@ -313,12 +373,22 @@ int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const vo
         while (k < a.npset && a.pset[k] != p_host[b]) ++k;
         if (k == a.npset && a.npset < kMaxSets) a.pset[a.npset++] = p_host[b];
         a.set_of[b] = k < a.npset ? k : -1;
+        if (a.set_of[b] < 0) a.overflow = 1;
     }
-    const int grid = num_sms() * 2;
     const size_t smem = sizeof(GemmSmem);
     auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGWarps * 32, smem);
+        if (e != cudaSuccess) return e;
+        // CTAs share a slice (its X staged once); slices get equal CTA counts
+        const int G = num_sms() * (per_sm > 0 ? per_sm : 1);
+        const int tile_groups = (int)ceil_div(a.NRT, kGWarps);
+        a.cps = G / a.NS > 1 ? G / a.NS : 1;
+        if (a.cps > tile_groups) a.cps = tile_groups;
+        const int units = a.NS * a.cps;
+        const int grid = units < G ? units : G;
         kern<<<grid, kGWarps * 32, smem, st>>>(a);
         return cudaGetLastError();
     };

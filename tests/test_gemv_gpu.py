@@ -344,3 +344,23 @@ def test_gemm_mixedp_matches_per_request_oracle(P, rows, cols, asym):
             z16 = None if z is None else z.astype(np.float16).astype(np.float32)
             want = O.gemv_lut(m.bitplanes.words, cols, 128, a16, z16, p, Xh[b])
             assert O.rel_dev(Y[b], want) <= 1e-4, (B, b, p, O.rel_dev(Y[b], want))
+
+
+@pytest.mark.parametrize("scale_dtype", ["f16", "f32"])
+def test_gemm_mixedp_deep_precisions(P, scale_dtype):
+    """p_max > 4 (planes staged in two rounds), more than kMaxSets distinct
+    precisions in one batch (global scale loads), f32 scale sets, and a cols
+    value that is not a multiple of 8 (scalar X staging)."""
+    rows, cols = 200, 1000
+    m = synth_model(P, rows, cols, 1, 7, asym=False, seed=5)
+    dm = P.DeviceModel.from_model(m, scale_dtype=scale_dtype)
+    ps = [1 + b % 7 for b in range(16)]
+    X = np.stack([O.random_gaussian(1, cols, seed=200 + b).ravel() for b in range(16)])
+    Xh = X.astype(np.float16).astype(np.float32)
+    Y = dm.gemm_mixedp(ps, torch.from_numpy(Xh).cuda()).cpu().numpy()
+    for b, p in enumerate(ps):
+        a = m.scale_sets[p].alpha
+        if scale_dtype == "f16":
+            a = a.astype(np.float16).astype(np.float32)
+        want = O.gemv_lut(m.bitplanes.words, cols, 128, a, None, p, Xh[b])
+        assert O.rel_dev(Y[b], want) <= 1e-4, (b, p, O.rel_dev(Y[b], want))

@@ -1,72 +1,37 @@
-"""Mixed-precision small-batch GEMM timing on the Llama-3-8B MLP block
-(gate/up 14336x4096, down 4096x14336), B in {1,2,4,8,16}, p pattern 2,3,4,...:
-tensor-core GEMM (one pass over the planes) vs B batched LUT GEMV jobs.
-
-    python tools/gemm_probe.py
-"""
+"""Time (and, under ncu, capture) the mixed-precision tensor-core GEMM on one
+Llama-3-8B MLP matrix: python tools/gemm_probe.py [--rows 14336] [--cols 4096] [--B 16] [--iters 50]"""
+import argparse
 import sys
 from pathlib import Path
 
-import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2510_10467_b200 as P  # noqa: E402
-from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
-from oracle import anybcq_oracle as O  # noqa: E402  (synthetic input generator)
 
-torch.cuda.set_device(0)
-SHAPES = [("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-COPIES = 2
-models = {}
-for name, r, c in SHAPES:
-    models[name] = []
-    for k in range(COPIES):
-        dm = P.DeviceModel(r, c, 128, 2, 4, scale_dtype="f16")
-        dm.load_planes(O.random_words(4, r, c, seed=k * 10 + r))
-        for p in (2, 3, 4):
-            dm.load_scale_set(p, np.full((p, r, c // 128), 0.05, np.float32))
-        models[name].append(dm)
-st = torch.cuda.Stream()
-
-
-def timeit(fn, reps=10):
-    with torch.cuda.stream(st):
-        fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=st):
-        fn()
-    with torch.cuda.stream(st):
-        g.replay()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        for _ in range(reps):
-            g.replay()
-        b.record(st)
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) * 1e3 / reps
-
-
-for B in (1, 2, 4, 8, 16):
-    ps = [2 + b % 3 for b in range(B)]
-    pmax = max(ps)
-    X = {c: torch.randn(B, c, device="cuda").half() for _, _, c in SHAPES}
-    outs = {n: torch.empty(B, r, device="cuda", dtype=torch.float16) for n, r, _ in SHAPES}
-
-    def gemm():
-        for k in range(COPIES):
-            for n, r, c in SHAPES:
-                models[n][k].gemm_mixedp(ps, X[c], out_dtype=torch.float16, stream=st)
-
-    def lut_jobs():
-        for k in range(COPIES):
-            for n, r, c in SHAPES:
-                gemv_batch([(models[n][k], ps[b], X[c][b], outs[n][b]) for b in range(B)], st)
-
-    t_g = timeit(gemm) / COPIES
-    t_l = timeit(lut_jobs) / COPIES
-    plane_bytes = sum(pmax * r * c // 8 for _, r, c in SHAPES)
-    print(f"B={B:2d} p={ps}: tensor-core GEMM {t_g:7.1f} us/MLP block ({plane_bytes / t_g / 1e3:6.0f} GB/s of planes, "
-          f"{B * 1e6 / t_g:8.0f} req-blocks/s) | {B} LUT jobs {t_l:7.1f} us")
+ap = argparse.ArgumentParser()
+ap.add_argument("--rows", type=int, default=14336)
+ap.add_argument("--cols", type=int, default=4096)
+ap.add_argument("--B", type=int, default=16)
+ap.add_argument("--iters", type=int, default=50)
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+gen = torch.Generator(device="cuda").manual_seed(0)
+dm = P.DeviceModel(a.rows, a.cols, 128, 2, 4, False, scale_dtype="f16")
+dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, a.rows, a.cols // 32), dtype=torch.int32, device=dev, generator=gen))
+for p in (2, 3, 4):
+    dm.load_scale_set(p, 0.01 + 0.1 * torch.randn(p, a.rows, a.cols // 128, device=dev, generator=gen).abs())
+ps = [(2, 3, 4)[b % 3] for b in range(a.B)]
+X = torch.randn(a.B, a.cols, device=dev).half()
+for _ in range(3):
+    dm.gemm_mixedp(ps, X)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.iters):
+    dm.gemm_mixedp(ps, X)
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / a.iters
+bits = max(ps) * a.rows * a.cols
+print(f"gemm {a.rows}x{a.cols} B={a.B} pmax={max(ps)}: {us:.2f} us/call, {bits / 8 / us / 1e3:.1f} GB/s of planes")

@@ -48,6 +48,8 @@ template <int NJ>
 struct KArgs {
     Job jobs[NJ];
     int cta_it[kMaxGrid + 1];  // CTA b owns batch items [cta_it[b], cta_it[b+1]) (host-computed)
+    uint32_t cta_split[kMaxGrid];      // CTA b: bit j set = its range touches split job j (host-computed)
+    unsigned char cta_j0[kMaxGrid];    // CTA b: job of its first item (job scans start there)
     int main_ctas;             // GEMV CTAs; CTAs beyond them complete the split-K sums
     int n_jobs;
     int total_items;
@@ -60,6 +62,8 @@ struct KArgs {
 struct BatchArgs {
     Job jobs[kMaxJobs];
     int cta_it[kMaxGrid + 1];
+    uint32_t cta_split[kMaxGrid];      // CTA b: bit j set = its range touches split job j (host-computed)
+    unsigned char cta_j0[kMaxGrid];    // CTA b: job of its first item (job scans start there)
     int main_ctas;
     int n_jobs;
     int total_items;
@@ -110,7 +114,7 @@ struct WarpRun {
 template <int NJ>
 __device__ __forceinline__ Piece piece_at(const KArgs<NJ>& a, int g, int it1) {
     Piece P;
-    P.j = 0;
+    P.j = a.cta_j0[blockIdx.x];  // g >= this CTA's first item: no scan from job 0 (param-space loads miss)
     while (P.j + 1 < a.n_jobs && a.jobs[P.j + 1].ibase <= g) ++P.j;
     const Job& J = a.jobs[P.j];
     P.s = (g - J.ibase) / J.NRT;
@@ -179,13 +183,21 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
     }
 }
 
-constexpr int kReduceRows = 512;  // rows per block of the standalone reduce kernel (1024 threads)
+constexpr int kReduceTPR = 2;  // threads per row: thread h sums chains 2h, 2h+1
+constexpr int kReduceThreads = 1024;
+constexpr int kReduceRows = kReduceThreads / kReduceTPR;  // rows per block of the standalone reduce kernel
+// (one block per 512 rows keeps the bench batch's reduce within the 2 x 148
+// blocks that are resident at once: a block that must wait for a free SM
+// lengthens the tail)
 
 // one reduce block: rows [blk*RPB, (blk+1)*RPB) of the blk-th block's job
-// (blocks laid out job by job), two threads per row (blockDim.x == 2*RPB)
-template <int NJ, typename YT, int RPB>
+// (blocks laid out job by job), kReduceTPR threads per row (blockDim.x == kReduceTPR*RPB).
+// RELEASE: let the dependent grid launch once this block's job has arrived --
+// not earlier, or the next kernel's CTAs take the SMs that the remaining
+// reduce blocks of this grid still need.
+template <int NJ, typename YT, int RPB, bool RELEASE>
 __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
-    constexpr int rpb = RPB;  // rows per block (two threads per row)
+    constexpr int rpb = RPB;
     int j = 0, nbj = 0;
     for (; j < a.n_jobs; ++j) {
         const Job& J = a.jobs[j];
@@ -194,40 +206,55 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         if (blk < nbj) break;
         blk -= nbj;
     }
-    if (j >= a.n_jobs) return;
+    if (j >= a.n_jobs) {
+        if (RELEASE) pdl_launch_dependents();
+        return;
+    }
     const Job& J = a.jobs[j];
     // wait for this job's CTA arrivals only (acquire), so the reduction
     // overlaps the GEMV CTAs still streaming other jobs
     if (threadIdx.x == 0) {
+        if (a.trace && j < 32) atomicMax(&a.trace[156 * 8 + j], globaltimer());  // last task start of job j
         uint32_t seen;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
+        for (;;) {  // relaxed polling, one acquire fence once the count is complete
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(J.arrive) : "memory");
             if (seen >= (uint32_t)J.ncta) break;
-            __nanosleep(32);
+            __nanosleep(20);
         }
-        if (a.trace) atomicMin(&a.trace[148 * 8 + 1], globaltimer());
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (a.trace) {
+            const unsigned long long t = globaltimer();
+            atomicMin(&a.trace[148 * 8 + 1], t);
+            if (j < 32) atomicMax(&a.trace[164 * 8 + j], t);  // last block of job j past its wait
+        }
     }
     __syncthreads();
-    const int hh = threadIdx.x & 1;  // chains 2hh, 2hh+1
-    const int row = blk * rpb + (threadIdx.x >> 1);
+    if (RELEASE) pdl_launch_dependents();
+    constexpr int CPT = 4 / kReduceTPR;  // chains per thread
+    const int sub = threadIdx.x % kReduceTPR;
+    const int row = blk * rpb + threadIdx.x / kReduceTPR;
     const float* pp = partial_row(J, row < J.rows ? row : 0);
-    const int nblk = (J.NS + 15) / 16;  // 16-slice blocks (the padding unit)
-    float c[2] = {0.f, 0.f};
-    for (int b0 = 0; b0 < nblk; b0 += 2) {  // up to 16 loads in flight
+    const int nterm = 4 * ((J.NS + 15) / 16);  // terms per chain, zero-padded to whole 16-slice blocks
+    float c[CPT];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) c[q] = 0.f;
+    for (int b0 = 0; b0 < nterm; b0 += 16 / CPT) {  // 16 loads in flight
         float v[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {  // k: block b0 + k/8, term (k%8)/2 of chain 2hh + k%2
-            const int bb = b0 + (k >> 3);
-            const int s = bb * 16 + ((k & 7) >> 1) * 4 + 2 * hh + (k & 1);
-            v[k] = (bb < nblk && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
+        for (int k = 0; k < 16; ++k) {  // chain sub*CPT + k%CPT, term b0 + k/CPT
+            const int term = b0 + k / CPT, s = term * 4 + sub * CPT + k % CPT;
+            v[k] = (term < nterm && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
         }
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            if (b0 + (k >> 3) < nblk) c[k & 1] += v[k];
+            if (b0 + k / CPT < nterm) c[k % CPT] += v[k];
     }
-    const float mine = c[0] + c[1];  // hh=0: c0+c1, hh=1: c2+c3
-    const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-    if (hh == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(mine + other);
+    float tot = c[0];
+#pragma unroll
+    for (int q = 1; q < CPT; ++q) tot += c[q];  // CPT == 2: c0+c1 | c2+c3
+#pragma unroll
+    for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
+    if (sub == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(tot);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (a.trace) {  // profiling: last block end, per job
@@ -259,9 +286,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             // retire) -- for batches whose reduce fits one wave; larger ones
             // use the separate kernel (a trailing CTA needs a whole SM, and
             // the role's code in the kernel costs the streams ~7%)
-            pdl_launch_dependents();
             pdl_wait();  // (y may still be read by the previous kernel)
-            reduce_rows<NJ, YT, kBThreads / 2>(a, blockIdx.x - a.main_ctas);
+            reduce_rows<NJ, YT, kBThreads / kReduceTPR, true>(a, blockIdx.x - a.main_ctas);
             return;
         }
     }
@@ -385,6 +411,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     }
     pdl_wait();  // x, y and the workspace belong to the previous kernel
     pdl_launch_dependents();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
 
     const int half = lane >> 4, r = lane & 15;
     uint32_t rb[6];
@@ -458,11 +485,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     for (int rs = it0; rs < it1; ++round) {
         const Round Rd = make_round(a, rs, it1);
         if (round >= 2) {  // table of round `round` (built by the last warp of round-2)
-            if (ready[round & 1] < round) {
-                const unsigned long long t0 = a.trace ? globaltimer() : 0;
-                while (ready[round & 1] < round) __nanosleep(64);
-                if (a.trace && lane == 0) atomicAdd(&a.trace[blockIdx.x * 8 + 7], globaltimer() - t0);
-            }
+            while (ready[round & 1] < round) __nanosleep(64);
             __threadfence_block();
         }
         const WarpRun wr = warp_run(a, Rd, warp);
@@ -562,22 +585,11 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             run(std::integral_constant<int, 1>{});
         else
             run(std::integral_constant<int, 0>{});
-        if (round == 0) {  // round-boundary profile: first / last warp done with round 0
-            if (a.trace && lane == 0) {
-                const unsigned long long now = globaltimer();
-                atomicMax(&a.trace[blockIdx.x * 8 + 5], now);
-                atomicMin(&a.trace[blockIdx.x * 8 + 4], now);
-            }
-        }
         // done with round `round`; builders fill round+2's table into this half
         __syncwarp();
         if (lane == 0) atomicAdd((int*)&done[round & 1], 1);
         if (build_next) {
-            if (done[round & 1] < kWarps) {
-                const unsigned long long t0 = a.trace ? globaltimer() : 0;
-                while (done[round & 1] < kWarps) __nanosleep(32);
-                if (a.trace && lane == 0) atomicAdd(&a.trace[blockIdx.x * 8 + 1], globaltimer() - t0);
-            }
+            while (done[round & 1] < kWarps) __nanosleep(32);
             __threadfence_block();
 #pragma unroll
             for (int k = 0; k < 4; ++k) build_entries(bx, round & 1, lane, (warp & 3) * 4 + k);
@@ -602,18 +614,21 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     // of its CTAs arrived, while stragglers are still streaming other jobs
     // (per-warp release arrivals were measured slower: one hot counter)
     __syncthreads();
-    if (tid == 0 && it0 < it1) {
-        __threadfence();
-        for (int j = 0; j < a.n_jobs; ++j) {
-            const Job& J = a.jobs[j];
-            if (J.NS > 1 && it0 < J.ibase + J.items && it1 > J.ibase) atomicAdd(J.arrive, 1u);
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 5] = globaltimer();  // all warps done
+    if (warp == 0 && it0 < it1) {  // lane j signals job j (each lane: release fence, then its arrival)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (a.trace && lane == 0) a.trace[blockIdx.x * 8 + 1] = globaltimer();  // fence done
+        const uint32_t mask = a.cta_split[b];
+        for (int j = lane; j < a.n_jobs; j += 32) {
+            if ((mask >> j) & 1u) {
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.jobs[j].arrive) : "memory");
+                if (a.trace && j < 32) atomicMax(&a.trace[160 * 8 + j], globaltimer());  // last arrival
+            }
         }
     }
     if (a.trace && tid == 0) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[blockIdx.x * 8 + 6] = round;
-        (void)smid;
+        a.trace[blockIdx.x * 8 + 4] = globaltimer();  // CTA done (arrivals issued)
     }
 }
 
@@ -627,10 +642,9 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 // default folds these blocks into the GEMV grid itself (trailing CTAs,
 // gemv_batch_kernel) -- one launch per batch, no kernel boundary.
 template <int NJ, typename YT>
-__global__ void __launch_bounds__(2 * kReduceRows, 2) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {  // 2 blocks/SM
+__global__ void __launch_bounds__(kReduceThreads, 2) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
-    pdl_launch_dependents();
-    reduce_rows<NJ, YT, kReduceRows>(a, blockIdx.x);
+    reduce_rows<NJ, YT, kReduceRows, true>(a, blockIdx.x);
     pdl_wait();  // the GEMV grid (y of unsplit jobs) completes before this grid does
 }
 
@@ -641,14 +655,19 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     a.n_jobs = ba.n_jobs;
     a.main_ctas = grid;
     for (int i = 0; i <= grid && i <= kMaxGrid; ++i) a.cta_it[i] = ba.cta_it[i];
+    for (int i = 0; i < grid && i < kMaxGrid; ++i) {
+        a.cta_split[i] = ba.cta_split[i];
+        a.cta_j0[i] = ba.cta_j0[i];
+    }
     a.total_items = ba.total_items;
     a.total_units = ba.total_units;
     a.prefill = ba.prefill;
     a.dbg = ba.dbg;
     a.trace = ba.trace;
-    int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/2) per job)
+    int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/4) per job)
+    constexpr int kFusedRows = kBThreads / kReduceTPR;
     for (int j = 0; j < ba.n_jobs; ++j)
-        if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kBThreads / 2 - 1) / (kBThreads / 2);
+        if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kFusedRows - 1) / kFusedRows;
     constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
     const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
     auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>
@@ -697,7 +716,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
     if (nblocks == 0) return 0;
     cudaLaunchConfig_t rc = cfg;
-    rc.blockDim = dim3(2 * kReduceRows);
+    rc.blockDim = dim3(kReduceThreads);
     rc.gridDim = dim3((unsigned)nblocks);
     rc.dynamicSmemBytes = 0;
     return (int)cudaLaunchKernelEx(&rc, batch_reduce_kernel<NJ, YT>, a);

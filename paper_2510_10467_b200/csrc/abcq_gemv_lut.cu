@@ -26,7 +26,9 @@ static size_t partial_bytes(const abcq_model_t* m) {
     if (NS <= 1) return 0;
     return align256((size_t)NS * NRT * kTileRows * sizeof(float));  // split-K partials
 }
-constexpr size_t kCounterBytes = 2 * kMaxJobs * sizeof(uint32_t);  // per job: CTA arrivals, reduce blocks done
+constexpr int kCounterStride = 32;  // one 128-byte line per counter: spinning readers and arrivals of
+                                    // different jobs never share a line
+constexpr size_t kCounterBytes = 2 * kMaxJobs * kCounterStride * sizeof(uint32_t);  // per job: CTA arrivals, reduce blocks done
 
 // workspace of a job list: every split job's partials, then (if any job is
 // split) the self-resetting per-job counters -- zero-filled once before use
@@ -80,8 +82,8 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     for (int j = 0; j < n; ++j) {
         make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
         w += partial_bytes(models[j]);
-        a.jobs[j].arrive = counters ? counters + j : nullptr;
-        a.jobs[j].reduced = counters ? counters + kMaxJobs + j : nullptr;
+        a.jobs[j].arrive = counters ? counters + j * kCounterStride : nullptr;
+        a.jobs[j].reduced = counters ? counters + (kMaxJobs + j) * kCounterStride : nullptr;
         Job& J = a.jobs[j];
         J.ibase = items;
         J.ubase = units;
@@ -173,10 +175,18 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
         if (memo.size() > 4096) memo.clear();
         memo.emplace(key, std::vector<int>(a.cta_it, a.cta_it + grid + 1));
     }
+    for (int b = 0; b < grid; ++b) {
+        a.cta_split[b] = 0;
+        a.cta_j0[b] = 0;
+        while (a.cta_j0[b] + 1 < n && a.jobs[a.cta_j0[b] + 1].ibase <= a.cta_it[b]) ++a.cta_j0[b];
+    }
     for (int j = 0; j < n; ++j) {  // CTAs whose range touches job j (arrivals its reduce waits for)
         Job& J = a.jobs[j];
         for (int b = 0; b < grid; ++b)
-            if (a.cta_it[b] < J.ibase + J.items && a.cta_it[b + 1] > J.ibase && a.cta_it[b] < a.cta_it[b + 1]) ++J.ncta;
+            if (a.cta_it[b] < J.ibase + J.items && a.cta_it[b + 1] > J.ibase && a.cta_it[b] < a.cta_it[b + 1]) {
+                ++J.ncta;
+                if (J.NS > 1) a.cta_split[b] |= 1u << j;
+            }
     }
     a.prefill = g_prefill;
     a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22) ? g_dbg_mode : 0;

@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-constexpr int kTraceCtas = 160;  // per launch trace slot: 8 stamps per CTA
+constexpr int kTraceCtas = 168;  // per launch trace slot: 8 stamps per CTA
 
 constexpr int kMaxFastP = ABCQ_MAX_PLANES;
 constexpr int kTableBytes = 256 * 256;  // 256 t-rows x 64 cols x 4 B: two 32-col segments

@@ -20,7 +20,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336),
           ("gate70", 28672, 8192), ("down70", 8192, 28672)]  # (7, 8: 70B shapes)
-NAMES = ["start", "-", "tab0", "streamed", "r0first", "r0last"]
+NAMES = ["start", "fenced", "tab0", "streamed", "ctadone", "synced", "-", "pdlwait"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--p", type=int, default=3)
@@ -84,7 +84,7 @@ us = e0.elapsed_time(e1) * 1e3 / 60
 print(f"jobs {[LAYERS[li][0] for li in sel]} p={PS}: {us:.2f} us/launch, {byts / 1e6:.1f} MB -> "
       f"{byts / us / 1e3:.0f} GB/s")
 
-SL = 160 * 8
+SL = 168 * 8
 buf = torch.zeros(16 * SL, dtype=torch.int64, device="cuda")
 _lib.lib().abcq_debug_set_trace(buf.data_ptr())
 g3 = torch.cuda.CUDAGraph()
@@ -96,11 +96,10 @@ with torch.cuda.stream(st):
     g3.replay()
     torch.cuda.synchronize()
     buf.zero_()
-    buf.view(16, 160, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
-    buf.view(16, 160, 8)[:, :148, 4] = 1 << 62   # first warp done with round 0 (atomicMin)
+    buf.view(16, 168, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
     g3.replay()
 torch.cuda.synchronize()
-t = buf.view(16, 160, 8).cpu().numpy()
+t = buf.view(16, 168, 8).cpu().numpy()
 used = [k for k in range(16) if t[k, :148, 0].max() > 0]
 used.sort(key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min())
 t0 = t[used[0], :148, 0][t[used[0], :148, 0] > 0].min()
@@ -114,9 +113,13 @@ for k in used:
     red = t[k, 148, :3].astype(np.float64)
     if red[2] > 0:
         jobs = t[k].reshape(-1)[149 * 8:149 * 8 + 32].astype(np.float64)
-        row.append("reduce first %.2f pdl %.2f end %.2f (jobs %s)" % (
+        arr = t[k].reshape(-1)[160 * 8:160 * 8 + 32].astype(np.float64)
+        wpass = t[k].reshape(-1)[164 * 8:164 * 8 + 32].astype(np.float64)
+        tstart = t[k].reshape(-1)[156 * 8:156 * 8 + 32].astype(np.float64)
+        row.append("reduce first %.2f pdl %.2f end %.2f (jobs arrive/taskstart/wait/end %s)" % (
             (red[0] - t0) / 1e3, (red[1] - t0) / 1e3, (red[2] - t0) / 1e3,
-            " ".join(f"{(v - t0) / 1e3:.1f}" for v in jobs if v > 0)))
+            " ".join(f"{(arr[i] - t0) / 1e3:.1f}/{(tstart[i] - t0) / 1e3:.1f}/{(wpass[i] - t0) / 1e3:.1f}/{(v - t0) / 1e3:.1f}"
+                     for i, v in enumerate(jobs) if v > 0)))
     print("  " + " | ".join(row))
 # per-CTA detail of the last launch: stream duration (tab0 -> streamed) vs rounds
 T = t[used[-1], :148].astype(np.float64)

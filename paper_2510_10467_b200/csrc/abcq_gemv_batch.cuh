@@ -22,7 +22,6 @@ namespace abcq {
 constexpr int kMaxJobs = 32;
 constexpr int kWarps = 16;
 constexpr int kBThreads = kWarps * 32;
-constexpr int kK = 4;  // items per slot
 
 struct Job {
     const uint4* planes;
@@ -75,6 +74,9 @@ struct BatchArgs {
 
 template <typename ST, bool ASYM>
 struct SlotGeom {
+    // items per slot: 8 (per-slot wait/issue/cursor work amortised over 8
+    // blocks) where a 2-deep ring of them fits, else 4
+    static constexpr int kK = (sizeof(ST) == 4 && ASYM) ? 4 : 8;
     static constexpr int kW = kK * kBlockBytes;           // weights
     static constexpr int kA = kK * 32 * (int)sizeof(ST);  // scales of one plane
     static constexpr int kZ = ASYM ? kK * 32 * (int)sizeof(ST) : 0;
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         }
     }
     using SG = SlotGeom<ST, ASYM>;
+    constexpr int kK = SG::kK;
     constexpr int R = SG::kRing;
     extern __shared__ __align__(1024) char smem[];
     // shared-memory map (window addresses): [base, 0x10000) = barriers, chunk
@@ -529,32 +532,43 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                         // a slot's kK elements are independent: load them all, then
                         // look up -- no per-element branch in the full-slot case, so
                         // the scheduler interleaves the four lookup chains
-                        auto elems = [&](auto n_tag) {
-                            constexpr int N = decltype(n_tag)::value;
+                        auto elems = [&](auto q0_tag, auto n_tag) {  // items [Q0, Q0 + N) of the slot
+                            constexpr int Q0 = decltype(q0_tag)::value, N = decltype(n_tag)::value;
                             uint4 wv[N];
                             float sc[N];
 #pragma unroll
                             for (int q = 0; q < N; ++q) {
-                                wv[q] = *reinterpret_cast<const uint4*>(st + q * kBlockBytes + lane * 16);
-                                sc[q] = to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW)[q * 32 + lane]);
+                                wv[q] = *reinterpret_cast<const uint4*>(st + (Q0 + q) * kBlockBytes + lane * 16);
+                                sc[q] = to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW)[(Q0 + q) * 32 + lane]);
                             }
 #pragma unroll
-                            for (int q = 0; q < N; ++q) acc[q] = fmaf(sc[q], lut16<SEG>(wv[q], rb), acc[q]);
+                            for (int q = 0; q < N; ++q) acc[Q0 + q] = fmaf(sc[q], lut16<SEG>(wv[q], rb), acc[Q0 + q]);
                             if constexpr (ASYM) {
                                 if (i == 0) {
 #pragma unroll
                                     for (int q = 0; q < N; ++q)
-                                        acc[q] = fmaf(to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW + SG::kA)[q * 32 + lane]),
-                                                      gx, acc[q]);
+                                        acc[Q0 + q] = fmaf(
+                                            to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW + SG::kA)[(Q0 + q) * 32 + lane]),
+                                            gx, acc[Q0 + q]);
                                 }
                             }
                         };
+                        using I0 = std::integral_constant<int, 0>;
+                        using I4 = std::integral_constant<int, 4>;
+                        auto group = [&](auto q0_tag, int n) {  // n = 1..4 items from Q0
+                            if (n == 4) elems(q0_tag, I4{});
+                            else if (n == 3) elems(q0_tag, std::integral_constant<int, 3>{});
+                            else if (n == 2) elems(q0_tag, std::integral_constant<int, 2>{});
+                            else elems(q0_tag, std::integral_constant<int, 1>{});
+                        };
                         if (cnt == kK) {
-                            elems(std::integral_constant<int, kK>{});
+                            elems(I0{}, I4{});
+                            if constexpr (kK == 8) elems(I4{}, I4{});
                         } else {
-                            if (cnt == 1) elems(std::integral_constant<int, 1>{});
-                            else if (cnt == 2) elems(std::integral_constant<int, 2>{});
-                            else elems(std::integral_constant<int, 3>{});
+                            group(I0{}, cnt < 4 ? cnt : 4);
+                            if constexpr (kK == 8) {
+                                if (cnt > 4) group(I4{}, cnt - 4);
+                            }
                         }
                     }
                     __syncwarp();  // every lane has consumed slot s

@@ -310,6 +310,7 @@ class DeviceModel:
 
 
 _BATCH_WS: dict = {}
+_BATCH_PLAN: dict = {}  # job-list key -> (ctypes job array, workspace, models)
 
 
 def gemv_batch(jobs, stream=None):
@@ -330,6 +331,17 @@ def gemv_batch(jobs, stream=None):
         for i in range(0, n, step):
             outs += gemv_batch(jobs[i:i + step], stream)
         return outs
+    # repeated job lists (a serving loop, a decoder step) skip the per-job
+    # validation and ctypes marshalling: same models, precisions, buffers
+    sh = _stream_handle(stream)
+    pkey = (sh, tuple((id(dm), p, x.data_ptr(), x.dtype, x.numel(), x.is_contiguous(),
+                      out.data_ptr(), out.dtype, out.numel(), out.is_contiguous())
+                     for dm, p, x, out in jobs))
+    hit = _BATCH_PLAN.get(pkey)
+    if hit is not None and not any(dm._level_ready for dm, _, _, _ in jobs):
+        arr, ws, _models = hit
+        _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
+        return [j[3] for j in jobs]
     arr = (_lib.AbcqGemvJob * n)()
     keep = []
     for k, (dm, p, x, out) in enumerate(jobs):
@@ -355,5 +367,9 @@ def gemv_batch(jobs, stream=None):
     if ws is None or ws.numel() < need.value:
         ws = torch.zeros(max(int(need.value), 16), dtype=torch.uint8, device=dev)
         _BATCH_WS[key] = ws
-    _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv_batch")
+    _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
+    if all(j[2].is_contiguous() for j in jobs):
+        if len(_BATCH_PLAN) > 256:
+            _BATCH_PLAN.clear()
+        _BATCH_PLAN[pkey] = (arr, ws, [j[0] for j in jobs])  # (models kept alive: id() stays unique)
     return [j[3] for j in jobs]

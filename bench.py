@@ -235,20 +235,32 @@ def run_gpu(args):
         torch.cuda.synchronize()
         return a0.elapsed_time(a1) / reps
 
-    # warm up (allocates per-stream workspaces), then capture one step as a graph
+    # warm up (allocates per-stream workspaces), then capture the K timed steps
+    # as CUDA graphs of up to 50 consecutive steps each (a graph per step would
+    # leave a replay gap between steps)
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             step_launches()
     torch.cuda.synchronize()
     use_graph = world == 1
-    graph = None
+    plan = []  # (graph, steps in it), replayed in order: exactly K steps
     if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            step_launches()
+        per = min(args.steps, 50)
+        sizes = [per] * (args.steps // per) + ([args.steps % per] if args.steps % per else [])
+        built = {}
+        for n in sizes:
+            if n not in built:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(n):
+                        step_launches()
+                built[n] = g
+            plan.append((built[n], n))
         with torch.cuda.stream(stream):
+            for g in built.values():  # (untimed: first replays)
+                g.replay()
             for _ in range(args.warmup):
-                graph.replay()
+                step_launches()
         torch.cuda.synchronize()
 
     # ---- timed region: K steps, events on the launching stream ------------
@@ -261,10 +273,11 @@ def run_gpu(args):
         clk.mark(True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for _ in range(args.steps):
-                if use_graph:
-                    graph.replay()
-                else:
+            if use_graph:
+                for g, _ in plan:
+                    g.replay()
+            else:
+                for _ in range(args.steps):
                     step_launches()
             ev1.record(stream)
         torch.cuda.synchronize()
@@ -415,7 +428,7 @@ def run_gpu(args):
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
                              f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
-                       "timing": "CUDA graph of one step, CUDA events on the launch stream",
+                       "timing": "the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream",
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
             # per step: the persistent batched GEMV kernel + the split-K reduce kernel
             "gpu_launches": args.steps * 2,

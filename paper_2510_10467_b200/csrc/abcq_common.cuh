@@ -129,6 +129,15 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     return r;
 }
 
+// ... with an L2 cache-policy hint (e.g. evict-first after the read)
+__device__ __forceinline__ uint4 ldg_stream_hint(const uint4* p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+
 }  // namespace abcq
 
 namespace abcq {

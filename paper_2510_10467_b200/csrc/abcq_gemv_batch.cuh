@@ -72,12 +72,14 @@ struct BatchArgs {
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
 };
 
-template <typename ST, bool ASYM>
+template <typename ST, bool ASYM, bool DIRECT = false>
 struct SlotGeom {
     // items per slot: 8 (per-slot wait/issue/cursor work amortised over 8
     // blocks) where a 2-deep ring of them fits, else 4
-    static constexpr int kK = (sizeof(ST) == 4 && ASYM) ? 4 : 8;
-    static constexpr int kW = kK * kBlockBytes;           // weights
+    static constexpr int kK = (!DIRECT && sizeof(ST) == 4 && ASYM) ? 4 : 8;
+    // DIRECT: weights are prefetched into L2 by the slot issue and loaded
+    // straight to registers at consumption; the slots stage only the scales
+    static constexpr int kW = DIRECT ? 0 : kK * kBlockBytes;  // weights
     static constexpr int kA = kK * 32 * (int)sizeof(ST);  // scales of one plane
     static constexpr int kZ = ASYM ? kK * 32 * (int)sizeof(ST) : 0;
     static constexpr int kBytes = kW + kA + kZ;
@@ -85,7 +87,8 @@ struct SlotGeom {
     // [0x20000, 227 KiB - 0x400 of dynamic smem)
     static constexpr int kLow = (int)((kTableWindow - 0x400 - 1024) / kBytes);
     static constexpr int kHigh = (227 * 1024 - (int)(2 * kTableWindow - 0x400)) / kBytes;
-    static constexpr int kRing = (kLow + kHigh) / kWarps < 6 ? (kLow + kHigh) / kWarps : 6;
+    static constexpr int kCap = DIRECT ? 4 : 6;
+    static constexpr int kRing = (kLow + kHigh) / kWarps < kCap ? (kLow + kHigh) / kWarps : kCap;
     static constexpr int kSmem =
         (int)(2 * kTableWindow - 0x400) + (kWarps * kRing > kLow ? kWarps * kRing - kLow : 0) * kBytes;
 };
@@ -187,17 +190,18 @@ __device__ __forceinline__ void lut_chunk_column16(const float (&xs)[8], int u, 
 
 constexpr int kReduceTPR = 2;  // threads per row: thread h sums chains 2h, 2h+1
 constexpr int kReduceThreads = 1024;
-constexpr int kReduceRows = kReduceThreads / kReduceTPR;  // rows per block of the standalone reduce kernel
-// (one block per 512 rows keeps the bench batch's reduce within the 2 x 148
-// blocks that are resident at once: a block that must wait for a free SM
-// lengthens the tail)
+constexpr int kReduceRPT = 2;  // rows per thread of the standalone reduce kernel
+constexpr int kReduceRows = kReduceThreads / kReduceTPR * kReduceRPT;  // rows per block
+// (few, fat blocks: the bench batch's reduce is one block per SM, and the
+// block dispatch of hundreds of 1024-thread blocks onto the SMs the GEMV
+// grid frees was measured at ~5 us)
 
 // one reduce block: rows [blk*RPB, (blk+1)*RPB) of the blk-th block's job
 // (blocks laid out job by job), kReduceTPR threads per row (blockDim.x == kReduceTPR*RPB).
 // RELEASE: let the dependent grid launch once this block's job has arrived --
 // not earlier, or the next kernel's CTAs take the SMs that the remaining
 // reduce blocks of this grid still need.
-template <int NJ, typename YT, int RPB, bool RELEASE>
+template <int NJ, typename YT, int RPB, int RPT, bool RELEASE>
 __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     constexpr int rpb = RPB;
     int j = 0, nbj = 0;
@@ -233,30 +237,45 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     __syncthreads();
     if (RELEASE) pdl_launch_dependents();
     constexpr int CPT = 4 / kReduceTPR;  // chains per thread
+    constexpr int kSpan = RPB / RPT;     // rows between a thread's rows
     const int sub = threadIdx.x % kReduceTPR;
-    const int row = blk * rpb + threadIdx.x / kReduceTPR;
-    const float* pp = partial_row(J, row < J.rows ? row : 0);
-    const int nterm = 4 * ((J.NS + 15) / 16);  // terms per chain, zero-padded to whole 16-slice blocks
-    float c[CPT];
+    int row[RPT];
+    const float* pp[RPT];
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) c[q] = 0.f;
-    for (int b0 = 0; b0 < nterm; b0 += 16 / CPT) {  // 16 loads in flight
-        float v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {  // chain sub*CPT + k%CPT, term b0 + k/CPT
-            const int term = b0 + k / CPT, s = term * 4 + sub * CPT + k % CPT;
-            v[k] = (term < nterm && s < J.NS) ? __ldcg(pp + s * kTileRows) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (b0 + k / CPT < nterm) c[k % CPT] += v[k];
+    for (int q = 0; q < RPT; ++q) {
+        row[q] = blk * rpb + q * kSpan + threadIdx.x / kReduceTPR;
+        pp[q] = partial_row(J, row[q] < J.rows ? row[q] : 0);
     }
-    float tot = c[0];
+    const int nterm = 4 * ((J.NS + 15) / 16);  // terms per chain, zero-padded to whole 16-slice blocks
+    float c[RPT][CPT];
 #pragma unroll
-    for (int q = 1; q < CPT; ++q) tot += c[q];  // CPT == 2: c0+c1 | c2+c3
+    for (int q = 0; q < RPT; ++q)
 #pragma unroll
-    for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
-    if (sub == 0 && row < J.rows) static_cast<YT*>(J.y)[row] = from_f32<YT>(tot);
+        for (int u = 0; u < CPT; ++u) c[q][u] = 0.f;
+    for (int b0 = 0; b0 < nterm; b0 += 16 / CPT) {  // 16 loads per row in flight
+        float v[RPT][16];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {  // chain sub*CPT + k%CPT, term b0 + k/CPT
+                const int term = b0 + k / CPT, s = term * 4 + sub * CPT + k % CPT;
+                v[q][k] = (term < nterm && s < J.NS) ? __ldcg(pp[q] + s * kTileRows) : 0.f;
+            }
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (b0 + k / CPT < nterm) c[q][k % CPT] += v[q][k];
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        float tot = c[q][0];
+#pragma unroll
+        for (int u = 1; u < CPT; ++u) tot += c[q][u];  // CPT == 2: c0+c1 | c2+c3
+#pragma unroll
+        for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
+        if (sub == 0 && row[q] < J.rows) static_cast<YT*>(J.y)[row[q]] = from_f32<YT>(tot);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (a.trace) {  // profiling: last block end, per job
@@ -280,7 +299,7 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
     } while (0)
 
-template <int NJ, typename XT, typename YT, typename ST, bool ASYM, bool FUSED>
+template <int NJ, typename XT, typename YT, typename ST, bool ASYM, bool FUSED, bool DIRECT>
 __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_constant__ KArgs<NJ> a) {
     if constexpr (FUSED) {
         if ((int)blockIdx.x >= a.main_ctas) {
@@ -289,11 +308,11 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             // use the separate kernel (a trailing CTA needs a whole SM, and
             // the role's code in the kernel costs the streams ~7%)
             pdl_wait();  // (y may still be read by the previous kernel)
-            reduce_rows<NJ, YT, kBThreads / kReduceTPR, true>(a, blockIdx.x - a.main_ctas);
+            reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true>(a, blockIdx.x - a.main_ctas);
             return;
         }
     }
-    using SG = SlotGeom<ST, ASYM>;
+    using SG = SlotGeom<ST, ASYM, DIRECT>;
     constexpr int kK = SG::kK;
     constexpr int R = SG::kRing;
     extern __shared__ __align__(1024) char smem[];
@@ -396,8 +415,13 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         const uint32_t wb = cnt * kBlockBytes, ab = cnt * 32 * (uint32_t)sizeof(ST);
         const bool z = ASYM && k.i == 0;
         if (lane == 0) {
-            mbar_arrive_expect_tx(&mybar[s], wb + ab + (z ? ab : 0));
-            bulk_g2s_hint(st, k.w, wb, &mybar[s], pol);
+            if constexpr (DIRECT) {
+                prefetch_l2_bulk(k.w, wb);
+                mbar_arrive_expect_tx(&mybar[s], ab + (z ? ab : 0));
+            } else {
+                mbar_arrive_expect_tx(&mybar[s], wb + ab + (z ? ab : 0));
+                bulk_g2s_hint(st, k.w, wb, &mybar[s], pol);
+            }
             bulk_g2s_hint(st + SG::kW, k.al, ab, &mybar[s], pol);
             if (z) bulk_g2s_hint(st + SG::kW + SG::kA, k.z, ab, &mybar[s], pol);
         }
@@ -519,6 +543,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             float* __restrict__ part = J.partial + (int64_t)P.s * kTileRows;  // + rt*NS*16 + r
             const int tile0 = J.ibase + P.s * J.NRT;  // batch item of row tile 0 of this slice
             const int p = J.p, NS = J.NS, rows = J.rows;
+            const int64_t pst = J.plane_stride_u4 * 16;
             for (int c = lo; c < hi; c += kK) {
                 const int cnt = min(kK, hi - c);
                 float acc[kK];
@@ -528,6 +553,9 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                     const int s = e % R;
                     mbar_wait(&mybar[s], (e / R) & 1);
                     const char* st = slot_ptr(warp * R + s);
+                    // DIRECT: this slot's weights in global memory (L2-resident by now)
+                    const char* wg = reinterpret_cast<const char*>(J.planes) + (int64_t)i * pst +
+                                     (int64_t)(c - J.ibase) * kBlockBytes + lane * 16;
                     if (a.dbg != 1) {
                         // a slot's kK elements are independent: load them all, then
                         // look up -- no per-element branch in the full-slot case, so
@@ -538,7 +566,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                             float sc[N];
 #pragma unroll
                             for (int q = 0; q < N; ++q) {
-                                wv[q] = *reinterpret_cast<const uint4*>(st + (Q0 + q) * kBlockBytes + lane * 16);
+                                if constexpr (DIRECT) wv[q] = ldg_stream_hint(reinterpret_cast<const uint4*>(wg + (Q0 + q) * kBlockBytes), pol);
+                                else wv[q] = *reinterpret_cast<const uint4*>(st + (Q0 + q) * kBlockBytes + lane * 16);
                                 sc[q] = to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW)[(Q0 + q) * 32 + lane]);
                             }
 #pragma unroll
@@ -656,9 +685,9 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 // default folds these blocks into the GEMV grid itself (trailing CTAs,
 // gemv_batch_kernel) -- one launch per batch, no kernel boundary.
 template <int NJ, typename YT>
-__global__ void __launch_bounds__(kReduceThreads, 2) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
+__global__ void __launch_bounds__(kReduceThreads, 1) batch_reduce_kernel(const __grid_constant__ KArgs<NJ> a) {
     if (a.trace && threadIdx.x == 0) atomicMin(&a.trace[148 * 8 + 0], globaltimer());
-    reduce_rows<NJ, YT, kReduceRows, true>(a, blockIdx.x);
+    reduce_rows<NJ, YT, kReduceRows, kReduceRPT, true>(a, blockIdx.x);
     pdl_wait();  // the GEMV grid (y of unsplit jobs) completes before this grid does
 }
 
@@ -684,33 +713,43 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kFusedRows - 1) / kFusedRows;
     constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
     const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
-    auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>
-                      : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>;
-    constexpr int smem = SlotGeom<ST, ASYM>::kSmem;
-    static_assert(smem <= 227 * 1024, "shared memory budget");
-    static_assert(SlotGeom<ST, ASYM>::kRing >= 2, "ring too shallow");
+    const bool direct = ba.dbg == 5;  // experiment: weights via L2 prefetch + direct loads
+    auto pick = [&](auto direct_tag) {
+        constexpr bool D = decltype(direct_tag)::value;
+        return fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, D> : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, D>;
+    };
+    auto kern = direct ? pick(std::true_type{}) : pick(std::false_type{});
+    const int smem = direct ? SlotGeom<ST, ASYM, true>::kSmem : SlotGeom<ST, ASYM>::kSmem;
+    static_assert(SlotGeom<ST, ASYM>::kSmem <= 227 * 1024, "shared memory budget");
+    static_assert(SlotGeom<ST, ASYM>::kRing >= 2 && SlotGeom<ST, ASYM, true>::kRing >= 2, "ring too shallow");
     int dev = 0;
     cudaGetDevice(&dev);
-    static bool attr_set[64] = {};  // per instantiation and device
-    if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return (int)e;
+    static bool attr_set[2][64] = {};  // per instantiation, variant and device
+    if (dev < 64 && !attr_set[direct][dev]) {
         // the reduce kernel keeps the GEMV's shared-memory carveout: an SM that
         // ran it must not be reconfigured before the next GEMV CTA can start
-        e = cudaFuncSetAttribute(batch_reduce_kernel<NJ, YT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
+        cudaError_t e = cudaFuncSetAttribute(batch_reduce_kernel<NJ, YT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return (int)e;
-        attr_set[dev] = true;
+        for (int f = 0; f < 2; ++f) {
+            auto kf = f ? kern : (direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, true>
+                                         : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, false>);
+            e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return (int)e;
+            e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return (int)e;
+        }
+        if (kCanFuse) {  // both fused variants of this direct setting
+            e = cudaFuncSetAttribute(direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, true>
+                                            : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return (int)e;
+            e = cudaFuncSetAttribute(direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, true>
+                                            : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, false>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return (int)e;
+        }
+        attr_set[direct][dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     const bool separate = !fused;

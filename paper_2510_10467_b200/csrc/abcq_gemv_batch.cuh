@@ -72,14 +72,14 @@ struct BatchArgs {
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
 };
 
-template <typename ST, bool ASYM, bool DIRECT = false>
+template <typename ST, bool ASYM>
 struct SlotGeom {
     // items per slot: 8 (per-slot wait/issue/cursor work amortised over 8
-    // blocks) where a 2-deep ring of them fits, else 4
-    static constexpr int kK = (!DIRECT && sizeof(ST) == 4 && ASYM) ? 4 : 8;
-    // DIRECT: weights are prefetched into L2 by the slot issue and loaded
-    // straight to registers at consumption; the slots stage only the scales
-    static constexpr int kW = DIRECT ? 0 : kK * kBlockBytes;  // weights
+    // blocks) where a 2-deep ring of them fits, else 4. (Weights loaded
+    // straight to registers after an L2 prefetch instead of TMA staging were
+    // measured 16% slower: the L2 latency lands on every slot.)
+    static constexpr int kK = (sizeof(ST) == 4 && ASYM) ? 4 : 8;
+    static constexpr int kW = kK * kBlockBytes;  // weights
     static constexpr int kA = kK * 32 * (int)sizeof(ST);  // scales of one plane
     static constexpr int kZ = ASYM ? kK * 32 * (int)sizeof(ST) : 0;
     static constexpr int kBytes = kW + kA + kZ;
@@ -87,8 +87,7 @@ struct SlotGeom {
     // [0x20000, 227 KiB - 0x400 of dynamic smem)
     static constexpr int kLow = (int)((kTableWindow - 0x400 - 1024) / kBytes);
     static constexpr int kHigh = (227 * 1024 - (int)(2 * kTableWindow - 0x400)) / kBytes;
-    static constexpr int kCap = DIRECT ? 4 : 6;
-    static constexpr int kRing = (kLow + kHigh) / kWarps < kCap ? (kLow + kHigh) / kWarps : kCap;
+    static constexpr int kRing = (kLow + kHigh) / kWarps < 6 ? (kLow + kHigh) / kWarps : 6;
     static constexpr int kSmem =
         (int)(2 * kTableWindow - 0x400) + (kWarps * kRing > kLow ? kWarps * kRing - kLow : 0) * kBytes;
 };
@@ -299,7 +298,7 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \
     } while (0)
 
-template <int NJ, typename XT, typename YT, typename ST, bool ASYM, bool FUSED, bool DIRECT>
+template <int NJ, typename XT, typename YT, typename ST, bool ASYM, bool FUSED>
 __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_constant__ KArgs<NJ> a) {
     if constexpr (FUSED) {
         if ((int)blockIdx.x >= a.main_ctas) {
@@ -312,7 +311,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             return;
         }
     }
-    using SG = SlotGeom<ST, ASYM, DIRECT>;
+    using SG = SlotGeom<ST, ASYM>;
     constexpr int kK = SG::kK;
     constexpr int R = SG::kRing;
     extern __shared__ __align__(1024) char smem[];
@@ -415,13 +414,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         const uint32_t wb = cnt * kBlockBytes, ab = cnt * 32 * (uint32_t)sizeof(ST);
         const bool z = ASYM && k.i == 0;
         if (lane == 0) {
-            if constexpr (DIRECT) {
-                prefetch_l2_bulk(k.w, wb);
-                mbar_arrive_expect_tx(&mybar[s], ab + (z ? ab : 0));
-            } else {
-                mbar_arrive_expect_tx(&mybar[s], wb + ab + (z ? ab : 0));
-                bulk_g2s_hint(st, k.w, wb, &mybar[s], pol);
-            }
+            mbar_arrive_expect_tx(&mybar[s], wb + ab + (z ? ab : 0));
+            bulk_g2s_hint(st, k.w, wb, &mybar[s], pol);
             bulk_g2s_hint(st + SG::kW, k.al, ab, &mybar[s], pol);
             if (z) bulk_g2s_hint(st + SG::kW + SG::kA, k.z, ab, &mybar[s], pol);
         }
@@ -543,7 +537,6 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             float* __restrict__ part = J.partial + (int64_t)P.s * kTileRows;  // + rt*NS*16 + r
             const int tile0 = J.ibase + P.s * J.NRT;  // batch item of row tile 0 of this slice
             const int p = J.p, NS = J.NS, rows = J.rows;
-            const int64_t pst = J.plane_stride_u4 * 16;
             for (int c = lo; c < hi; c += kK) {
                 const int cnt = min(kK, hi - c);
                 float acc[kK];
@@ -553,9 +546,6 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                     const int s = e % R;
                     mbar_wait(&mybar[s], (e / R) & 1);
                     const char* st = slot_ptr(warp * R + s);
-                    // DIRECT: this slot's weights in global memory (L2-resident by now)
-                    const char* wg = reinterpret_cast<const char*>(J.planes) + (int64_t)i * pst +
-                                     (int64_t)(c - J.ibase) * kBlockBytes + lane * 16;
                     if (a.dbg != 1) {
                         // a slot's kK elements are independent: load them all, then
                         // look up -- no per-element branch in the full-slot case, so
@@ -566,8 +556,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
                             float sc[N];
 #pragma unroll
                             for (int q = 0; q < N; ++q) {
-                                if constexpr (DIRECT) wv[q] = ldg_stream_hint(reinterpret_cast<const uint4*>(wg + (Q0 + q) * kBlockBytes), pol);
-                                else wv[q] = *reinterpret_cast<const uint4*>(st + (Q0 + q) * kBlockBytes + lane * 16);
+                                wv[q] = *reinterpret_cast<const uint4*>(st + (Q0 + q) * kBlockBytes + lane * 16);
                                 sc[q] = to_f32<ST>(reinterpret_cast<const ST*>(st + SG::kW)[(Q0 + q) * 32 + lane]);
                             }
 #pragma unroll
@@ -713,43 +702,26 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kFusedRows - 1) / kFusedRows;
     constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
     const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
-    const bool direct = ba.dbg == 5;  // experiment: weights via L2 prefetch + direct loads
-    auto pick = [&](auto direct_tag) {
-        constexpr bool D = decltype(direct_tag)::value;
-        return fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, D> : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, D>;
-    };
-    auto kern = direct ? pick(std::true_type{}) : pick(std::false_type{});
-    const int smem = direct ? SlotGeom<ST, ASYM, true>::kSmem : SlotGeom<ST, ASYM>::kSmem;
-    static_assert(SlotGeom<ST, ASYM>::kSmem <= 227 * 1024, "shared memory budget");
-    static_assert(SlotGeom<ST, ASYM>::kRing >= 2 && SlotGeom<ST, ASYM, true>::kRing >= 2, "ring too shallow");
+    auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse> : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>;
+    constexpr int smem = SlotGeom<ST, ASYM>::kSmem;
+    static_assert(smem <= 227 * 1024, "shared memory budget");
+    static_assert(SlotGeom<ST, ASYM>::kRing >= 2, "ring too shallow");
     int dev = 0;
     cudaGetDevice(&dev);
-    static bool attr_set[2][64] = {};  // per instantiation, variant and device
-    if (dev < 64 && !attr_set[direct][dev]) {
+    static bool attr_set[64] = {};  // per instantiation and device
+    if (dev < 64 && !attr_set[dev]) {
         // the reduce kernel keeps the GEMV's shared-memory carveout: an SM that
         // ran it must not be reconfigured before the next GEMV CTA can start
         cudaError_t e = cudaFuncSetAttribute(batch_reduce_kernel<NJ, YT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return (int)e;
-        for (int f = 0; f < 2; ++f) {
-            auto kf = f ? kern : (direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, true>
-                                         : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false, false>);
+        for (auto kf : {gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse>, gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>}) {
             e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return (int)e;
             e = cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return (int)e;
         }
-        if (kCanFuse) {  // both fused variants of this direct setting
-            e = cudaFuncSetAttribute(direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, true>
-                                            : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e != cudaSuccess) return (int)e;
-            e = cudaFuncSetAttribute(direct ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, true>
-                                            : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse, false>,
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-            if (e != cudaSuccess) return (int)e;
-        }
-        attr_set[direct][dev] = true;
+        attr_set[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     const bool separate = !fused;

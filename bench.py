@@ -106,7 +106,7 @@ class ClockSampler:
                 self.rows.append((sm, rs, time.perf_counter()))
             except Exception:
                 return
-            time.sleep(0.0005)
+            time.sleep(0)  # (yield the GIL; the timed region can be only a few ms long)
 
     def __enter__(self):
         if self.nvml is not None:
@@ -366,49 +366,79 @@ def run_gpu(args):
     # ---- e2e: public API with pinned host buffers, copies in the timed region
     e2e = None
     if rank == 0:
-        # one pinned staging buffer each way: x of both input widths in, the 21
-        # outputs out (views of one device buffer) -- one copy per direction
+        # one pinned staging buffer each way per step: x of both input widths
+        # in, the 21 outputs out (views of one device buffer) -- one copy per
+        # direction and step. Serving-style pipeline: two buffer sets, the H2D
+        # of step i+1 and the D2H of step i on their own streams overlap the
+        # GEMV launch of step i (event-ordered; every step still moves its
+        # own bytes both ways inside the timed region)
         kx = sorted(xs)
         hx = torch.cat([xs[k].cpu() for k in kx]).pin_memory()
-        dxa = torch.empty_like(hx, device=dev)
-        dx, off = {}, 0
-        for k in kx:
-            dx[k] = dxa[off:off + k]
-            off += k
         n_out = sum(models[pi][li].rows for pi, p, li in all_jobs)
-        dya = torch.empty(n_out, dtype=torch.float16, device=dev)
-        hya = torch.empty(n_out, dtype=torch.float16).pin_memory()
-        dys, off = [], 0
-        for pi, p, li in all_jobs:
-            dys.append(dya[off:off + models[pi][li].rows])
-            off += models[pi][li].rows
+        sets = []
+        for _ in range(2):
+            dxa = torch.empty_like(hx, device=dev)
+            dx, off = {}, 0
+            for k in kx:
+                dx[k] = dxa[off:off + k]
+                off += k
+            dya = torch.empty(n_out, dtype=torch.float16, device=dev)
+            dys, off = [], 0
+            for pi, p, li in all_jobs:
+                dys.append(dya[off:off + models[pi][li].rows])
+                off += models[pi][li].rows
+            sets.append({"dxa": dxa, "dx": dx, "dya": dya, "dys": dys,
+                         "hy": torch.empty(n_out, dtype=torch.float16).pin_memory(),
+                         "in": torch.cuda.Event(), "comp": torch.cuda.Event(), "out": torch.cuda.Event()})
+        for S in sets:  # the public API's repeated-launch form (validated and marshalled once)
+            S["plan"] = P.GemvBatchPlan([(models[pi][li], p, S["dx"][models[pi][li].cols], S["dys"][n])
+                                         for n, (pi, p, li) in enumerate(all_jobs)])
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         h2d = d2h = 0
 
-        def e2e_step():
+        def e2e_step(i):
             nonlocal h2d, d2h
-            dxa.copy_(hx, non_blocking=True)
+            S = sets[i & 1]
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(S["comp"])  # the GEMV that last read this x buffer is done
+                S["dxa"].copy_(hx, non_blocking=True)
+                S["in"].record(s_in)
             h2d += hx.numel() * 2
-            gemv_batch([(models[pi][li], p, dx[models[pi][li].cols], dys[n])
-                        for n, (pi, p, li) in enumerate(all_jobs)], stream)
-            hya.copy_(dya, non_blocking=True)
-            d2h += dya.numel() * 2
+            stream.wait_event(S["in"])
+            stream.wait_event(S["out"])  # the D2H that last read this y buffer is done
+            S["plan"].launch(stream)
+            S["comp"].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(S["comp"])
+                S["hy"].copy_(S["dya"], non_blocking=True)
+                S["out"].record(s_out)
+            d2h += S["dya"].numel() * 2
+
         with torch.cuda.stream(stream):
-            for _ in range(3):
-                e2e_step()
+            for S in sets:
+                for e in ("in", "comp", "out"):
+                    S[e].record(stream)
+            for i in range(4):
+                e2e_step(i)
             torch.cuda.synchronize()
             h2d = d2h = 0
-            n_e2e = max(3, min(args.steps, 20))
+            n_e2e = max(4, min(args.steps, 50))
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            for _ in range(n_e2e):
-                e2e_step()
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            for i in range(n_e2e):
+                e2e_step(i)
+            stream.wait_stream(s_out)
             b.record(stream)
             torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / n_e2e
         e2e = {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d // n_e2e,
                "d2h_bytes_per_step": d2h // n_e2e,
-               "api": "gemv_batch of the 21 GEMVs (C ABI abcq_gemv_batch); pinned host x in and y out, one copy each way"}
+               "api": "GemvBatchPlan.launch of the 21 GEMVs (one C-ABI abcq_gemv_batch call per step), eager; "
+                      "pinned host x in and y out, one copy each way per step, copies of neighbouring steps "
+                      "overlapped on two side streams"}
 
     if rank == 0:
         peak, peak_kind = read_peaks()

@@ -20,7 +20,7 @@ def __getattr__(name):
                 "render_bench_csv"):
         from . import engine
         return getattr(engine, name)
-    if name == "DeviceModel":
-        from .device_model import DeviceModel
-        return DeviceModel
+    if name in ("DeviceModel", "GemvBatchPlan", "gemv_batch"):
+        from . import device_model
+        return getattr(device_model, name)
     raise AttributeError(name)

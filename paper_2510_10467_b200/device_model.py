@@ -373,3 +373,50 @@ def gemv_batch(jobs, stream=None):
             _BATCH_PLAN.clear()
         _BATCH_PLAN[pkey] = (arr, ws, [j[0] for j in jobs])  # (models kept alive: id() stays unique)
     return [j[3] for j in jobs]
+
+
+class GemvBatchPlan:
+    """A job list validated and marshalled once, launched many times (a
+    serving loop or a decoder step over fixed buffers): `launch()` is one
+    C-ABI call (abcq_gemv_batch) with no per-call Python work on the jobs.
+
+    jobs: as for gemv_batch. The plan keeps the models and tensors alive; the
+    split-K workspace is per stream (zero-filled once, self-resetting).
+    """
+
+    def __init__(self, jobs):
+        L = _lib.lib()
+        self.n = len(jobs)
+        if not 0 < self.n <= L.abcq_gemv_batch_max_jobs():
+            raise UsageError(f"a plan holds 1..{L.abcq_gemv_batch_max_jobs()} jobs")
+        self.jobs = list(jobs)
+        self.arr = (_lib.AbcqGemvJob * self.n)()
+        for k, (dm, p, x, out) in enumerate(self.jobs):
+            dm._check_p(p)
+            if dm._check_x(x) is not x:
+                raise UsageError("plan inputs must be contiguous device tensors")
+            if out.numel() != dm.rows or not out.is_contiguous() or out.device != dm.device:
+                raise UsageError("out must be a contiguous device tensor of `rows` elements")
+            self.arr[k].model = C.pointer(dm._struct)
+            self.arr[k].p = p
+            self.arr[k].x_dtype = dtype_code(x.dtype)
+            self.arr[k].y_dtype = dtype_code(out.dtype)
+            self.arr[k].x = x.data_ptr()
+            self.arr[k].y = out.data_ptr()
+        need = C.c_size_t()
+        _lib.check(L.abcq_gemv_batch_workspace_bytes(self.arr, self.n, C.byref(need)), "abcq_gemv_batch")
+        self.need = max(int(need.value), 16)
+        self.device = self.jobs[0][0].device
+        self._ws = {}
+        self._L = L
+
+    def launch(self, stream=None):
+        for dm, p, _, _ in self.jobs:
+            if dm._level_ready:
+                dm._order_after_upload(p, stream)
+        sh = _stream_handle(stream)
+        ws = self._ws.get(sh)
+        if ws is None:
+            ws = self._ws[sh] = torch.zeros(self.need, dtype=torch.uint8, device=self.device)
+        _lib.check(self._L.abcq_gemv_batch(self.arr, self.n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
+        return [j[3] for j in self.jobs]

@@ -316,6 +316,30 @@ def test_gemv_batch_matches_single_calls(P):
         assert torch.equal(out, w)
 
 
+def test_gemv_batch_plan_repeated_launches(P):
+    """GemvBatchPlan (validated once, one C-ABI call per launch) == gemv_batch,
+    bitwise, over repeated launches on two streams (per-stream workspaces),
+    with the inputs changed in place between launches."""
+    from paper_2510_10467_b200.device_model import gemv_batch
+    shapes = [(4096, 4096), (1024, 4096), (14336, 4096)]
+    models = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r), scale_dtype="f16") for r, c in shapes]
+    x = torch.from_numpy(O.random_gaussian(1, 4096, seed=5).ravel()).cuda().half()
+    jobs = [(dm, p, x, torch.empty(dm.rows, device="cuda", dtype=torch.float16)) for dm in models for p in (2, 3, 4)]
+    plan = P.GemvBatchPlan(jobs)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for it in range(4):
+        x.copy_(torch.from_numpy(O.random_gaussian(1, 4096, seed=10 + it).ravel()).half())
+        torch.cuda.synchronize()
+        want = [o.clone() for o in gemv_batch([(dm, p, x, torch.empty_like(out)) for dm, p, _, out in jobs])]
+        with torch.cuda.stream(streams[it & 1]):
+            plan.launch(streams[it & 1])
+        torch.cuda.synchronize()
+        for (_, _, _, out), w in zip(jobs, want):
+            assert torch.equal(out, w)
+    with pytest.raises(P.UsageError):
+        P.GemvBatchPlan([(models[0], 5, x, jobs[0][3])])  # precision outside [p_lo, p_hi]
+
+
 def test_gemv_batch_asymmetric(P):
     from paper_2510_10467_b200.device_model import gemv_batch
     ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]

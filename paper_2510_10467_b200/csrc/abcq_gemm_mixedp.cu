@@ -55,6 +55,7 @@ struct GemmArgs {
     int overflow;           // some request's precision is not among pset (its scales are read from global)
     int rows, cols, NRT, NS, items, B, pmax;
     int cps;  // CTAs per slice (each takes every cps-th group of kGWarps row tiles)
+    int dbg;  // profiling experiments (tcgen05 kernel): 31 no MMA, 32 no TMEM store, 33 no TMEM load (unused: 0)
 };
 
 // dynamic shared memory of the GEMM kernel
@@ -343,6 +344,375 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ partial, int NS, in
     }
 }
 
+// ===========================================================================
+// tcgen05 variant (opt-in, abcq_debug_set_mode(40)): the expanded +-1 weights are the A operand in
+// TENSOR MEMORY, X (the batch, padded to 16 requests) the B operand in shared
+// memory, the accumulator D in TMEM. One CTA = 4 expander/epilogue warps
+// (thread = weight row = TMEM lane) + 1 MMA warp (one elected thread).
+//
+//   per step (one 128-column group g of one plane i of a 128-row block):
+//     expanders: 16 plane bytes of their row (cp.async ring, 8 steps deep) ->
+//       un-rotate -> 64 x f16x2 (+-1) -> tcgen05.st.32x32b.x64 into A[slot]
+//       -> mbarrier a_full[slot]
+//     MMA thread: 8 x tcgen05.mma.kind::f16 (M=128, N=16, K=16) A[slot] x
+//       X(g) -> D[slot] -> tcgen05.commit -> mbarrier d_full[slot]
+//     expanders (one step behind): tcgen05.ld D[slot] -> y_b += alpha^(p_b)
+//       [i,row,g] * D[row][b] for the requests with p_b > i -> d_empty[slot]
+//   A and D are double-buffered (TMEM columns A: 0 / 64, D: 128 / 144), so
+//   the expansion of step s overlaps the MMAs of step s-1.
+// K order inside a 32-column block is permuted so that one f16x2 takes bits
+// j and j+16 of a plane word (2 instructions per f16x2: shift + lop3); X is
+// staged in shared memory in the same order, in the canonical no-swizzle
+// K-major core-matrix layout (8 rows x 16 B; LBO = 256 B along K, SBO =
+// 128 B along N). Work item = (128-row block, 256-column slice); a CTA takes a
+// contiguous item range; per-slice partials [NS][B][rows] are summed by
+// gemm_reduce_kernel exactly as for the mma.sync kernel.
+// ===========================================================================
+namespace tcg {
+constexpr int kM = 128;
+constexpr int kN = 16;
+constexpr int kExp = 8;                   // expander / epilogue warps: 2 per TMEM lane quarter (K halves)
+constexpr int kThreads = (kExp + 1) * 32;
+constexpr int kSlots = 3;                 // A / D buffers: expansion runs up to 2 steps ahead of the epilogue
+constexpr uint32_t kTmemCols = 256;       // A[3]: 0, 64, 128; D[3]: 192, 208, 224
+constexpr uint32_t kDCol = 64 * kSlots;
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);  // f16.f16->f32
+constexpr int kXBytes = kN * 256 * 2;     // one slice of X (16 requests x 256 columns, f16)
+constexpr int kRing = 8;                  // weight steps in flight per thread (cp.async)
+struct Smem {
+    char x[2][kXBytes];                   // X of a slice, core-matrix layout; slice parity picks the buffer
+    uint4 wring[kRing][kExp * 32];        // per-thread weight ring
+    float gsum[2][2][kN][8];              // asymmetric: [xbuf][group][request][16-col part] sums of x
+    uint64_t a_full[kSlots], d_full[kSlots], d_empty[kSlots];
+    uint32_t tmem;
+};
+
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t bdesc(uint32_t addr) {  // K-major, no swizzle, LBO 256 B, SBO 128 B
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(256 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) |
+           ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+}  // namespace tcg
+
+template <typename ST, bool ASYM>
+__global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArgs a, int it_per_cta) {
+    using namespace tcg;
+    extern __shared__ __align__(1024) char tsm[];
+    Smem& S = *reinterpret_cast<Smem*>(tsm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int NRB = (a.NRT + 7) / 8;
+    const int n_items = NRB * a.NS;
+    const int it0 = blockIdx.x * it_per_cta;
+    const int it1 = min(n_items, it0 + it_per_cta);
+    const int spi = 2 * a.pmax;  // steps per item: group-major, plane-minor
+    const int nsteps = it1 > it0 ? (it1 - it0) * spi : 0;
+
+    if (warp == kExp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int k = 0; k < kSlots; ++k) {
+            mbar_init(&S.a_full[k], kExp * 32);
+            mbar_init(&S.d_full[k], 1);
+            mbar_init(&S.d_empty[k], kExp * 32);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = S.tmem;
+
+    if (warp == kExp) {
+        // ---- MMA issuer -------------------------------------------------------
+        if (lane == 0) {
+            for (int st = 0; st < nsteps; ++st) {
+                const int slot = st % kSlots;
+                const uint32_t ph = (st / kSlots) & 1;
+                mbar_wait(&S.a_full[slot], ph);
+                if (st >= kSlots) mbar_wait(&S.d_empty[slot], ph ^ 1);  // epilogue of step st - kSlots
+                tc_fence_after();
+                const int it = it0 + st / spi, r = st % spi, gl = r / a.pmax;
+                const int sl = it / NRB;
+                const uint32_t xaddr = smem_addr(S.x[sl & 1]) + gl * 8 * 512;
+                const uint32_t d_t = tbase + kDCol + 16 * slot, a_t = tbase + 64 * slot;
+                if (a.dbg == 31) {
+                    arrive(&S.d_full[slot]);
+                    continue;
+                }
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t bd = bdesc(xaddr + kk * 512);
+                    const uint32_t acc = kk > 0;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_t),
+                        "r"(a_t + 8 * kk), "l"(bd), "r"(kIdesc), "r"(acc)
+                        : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_addr(&S.d_full[slot]))
+                             : "memory");
+            }
+        }
+    } else {
+        // ---- expanders / epilogue: thread t = row t of the 128-row block ---------
+        // thread = (row t of the 128-row block, K half kh): warps w and w+4 share
+        // TMEM lane quarter w; kh picks 64 of the group's 128 columns (A columns
+        // [32kh, 32kh+32) of a slot) and 8 of the 16 requests in the epilogue
+        const int kh = warp >> 2, t = (warp & 3) * 32 + lane, r16 = t & 15, tib = t >> 4;
+        const int B = a.B;
+        const int64_t NRT16 = (int64_t)a.NRT * kTileRows;
+        const int64_t pst = a.plane_stride_u4;
+        constexpr int kNh = kN / 2;  // requests per thread: kh*8 .. kh*8+7
+        int sb[kNh];
+#pragma unroll
+        for (int b = 0; b < kNh; ++b) sb[b] = kh * kNh + b < B ? a.set_of[kh * kNh + b] : 0;
+        // step cursors (no divisions in the loop): item it = (slice sl, row block
+        // rb), group gl of the slice, plane i; steps run group-major, plane-minor
+        struct Pos {
+            int it, sl, rb, gl, i;
+        };
+        auto pos_at = [&](int st) {
+            Pos q;
+            const int item = st / spi, r = st - item * spi;
+            q.it = it0 + item;
+            q.sl = q.it / NRB;
+            q.rb = q.it - q.sl * NRB;
+            q.gl = r / a.pmax;
+            q.i = r - q.gl * a.pmax;
+            return q;
+        };
+        auto advance = [&](Pos& q) {
+            if (++q.i < a.pmax) return;
+            q.i = 0;
+            if (++q.gl < 2) return;
+            q.gl = 0;
+            ++q.it;
+            if (++q.rb == NRB) {
+                q.rb = 0;
+                ++q.sl;
+            }
+        };
+        // raw (unconverted) scales of a step: one per staged precision set; the
+        // conversion happens at the epilogue, two steps later, so the loads are
+        // never waited on in the step that issues them
+        struct Sc {
+            ST al[kMaxSets];
+            ST z[kMaxSets];
+        };
+        const ST zero = from_f32<ST>(0.f);
+        auto load_sc = [&](const Pos& q, bool live) {
+            Sc c;
+            const int tile = min(q.rb * 8 + tib, a.NRT - 1);
+            const int64_t e = (int64_t)(q.sl * a.NRT + tile) * 32 + q.gl * 16 + r16;
+#pragma unroll
+            for (int k = 0; k < kMaxSets; ++k) {
+                const int pk = k < a.npset ? a.pset[k] : 0;
+                c.al[k] = (live && q.i < pk) ? __ldg(static_cast<const ST*>(a.alpha[pk]) + (int64_t)q.i * a.items * 32 + e)
+                                             : zero;
+                if constexpr (ASYM)
+                    c.z[k] = (live && q.i == 0 && pk > 0) ? __ldg(static_cast<const ST*>(a.offset[pk]) + e) : zero;
+                else
+                    c.z[k] = zero;
+            }
+            return c;
+        };
+        auto wsrc = [&](const Pos& q, bool& valid) -> const uint4* {
+            const int tile = q.rb * 8 + tib;
+            valid = tile < a.NRT;
+            return a.planes + q.i * pst + ((int64_t)(q.sl * a.NRT + (valid ? tile : 0)) * 32 + q.gl * 16 + r16);
+        };
+        Pos wp = pos_at(0), cp = wp, sp = wp, ep = wp;
+        // prologue: weight ring (steps 0 .. kRing-2), scales of step 0
+        for (int k = 0; k < kRing - 1; ++k) {
+            bool v = false;
+            const uint4* src = k < nsteps ? wsrc(wp, v) : a.planes;
+            cp16(&S.wring[k][tid], src, k < nsteps && v);
+            cp_async_commit();
+            advance(wp);
+        }
+        Sc sc_e, sc_1, sc_2;  // after iteration st's rotation: scales of steps st-2 (epilogue), st-1, st
+        float acc[kNh];
+#pragma unroll
+        for (int b = 0; b < kNh; ++b) acc[b] = 0.f;
+        int staged = -1;
+        // X staging: request xn, 32-column block xcb, half xpt (kappa chunks 2xpt, 2xpt+1)
+        const int xn = tid >> 4, xcb = (tid >> 1) & 7, xpt = tid & 1;
+
+        auto epilogue = [&](int e) {
+            const int slot = e % kSlots;
+            mbar_wait(&S.d_full[slot], (e / kSlots) & 1);
+            tc_fence_after();
+            uint32_t d[8] = {};
+            if (a.dbg != 33)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+                : "r"(tbase + ((uint32_t)((warp & 3) * 32) << 16) + kDCol + 16 * slot + 8 * kh)
+                : "memory");
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            arrive(&S.d_empty[slot]);
+            // per-request coefficient: alpha of the request's precision set (already 0
+            // where the set's precision <= i); scalar selects, no indexed array (an
+            // indexed register array is spilled to local memory)
+            static_assert(kMaxSets == 4, "four scale sets");
+            const float a0 = to_f32<ST>(sc_e.al[0]), a1 = to_f32<ST>(sc_e.al[1]);
+            const float a2 = to_f32<ST>(sc_e.al[2]), a3 = to_f32<ST>(sc_e.al[3]);
+#pragma unroll
+            for (int b = 0; b < kNh; ++b) {
+                const int k = sb[b];
+                const float c = k < 2 ? (k == 0 ? a0 : a1) : (k == 2 ? a2 : a3);
+                acc[b] = fmaf(c, __uint_as_float(d[b]), acc[b]);
+            }
+            if constexpr (ASYM) {
+                if (ep.i == 0) {
+                    const float z0 = to_f32<ST>(sc_e.z[0]), z1 = to_f32<ST>(sc_e.z[1]);
+                    const float z2 = to_f32<ST>(sc_e.z[2]), z3 = to_f32<ST>(sc_e.z[3]);
+#pragma unroll
+                    for (int b = 0; b < kNh; ++b) {
+                        const float* gs = S.gsum[ep.sl & 1][ep.gl][kh * kNh + b];
+                        const float gx = ((gs[0] + gs[1]) + (gs[2] + gs[3])) + ((gs[4] + gs[5]) + (gs[6] + gs[7]));
+                        const int k = sb[b];
+                        const float z = k < 2 ? (k == 0 ? z0 : z1) : (k == 2 ? z2 : z3);
+                        acc[b] = fmaf(z, gx, acc[b]);
+                    }
+                }
+            }
+            if (ep.gl == 1 && ep.i == a.pmax - 1) {  // item done: this row's partial for the slice
+                const int tile = ep.rb * 8 + tib;
+                if (tile < a.NRT) {
+                    float* out = a.partial + ((int64_t)ep.sl * B + kh * kNh) * NRT16 + tile * kTileRows + r16;
+#pragma unroll
+                    for (int b = 0; b < kNh; ++b)
+                        if (kh * kNh + b < B) out[b * NRT16] = acc[b];
+                }
+#pragma unroll
+                for (int b = 0; b < kNh; ++b) acc[b] = 0.f;
+            }
+            advance(ep);
+        };
+
+        for (int st = 0; st < nsteps; ++st) {
+            const int slot = st % kSlots;
+            if (cp.gl == 0 && cp.i == 0 && cp.sl != staged) {  // stage X of this slice (B operand), permuted K order
+                staged = cp.sl;
+                char* xs = S.x[cp.sl & 1];
+                const int c0 = cp.sl * 256 + xcb * 32 + xpt * 8;  // columns c0 + [0,8) and c0 + 16 + [0,8)
+                __half v[16];
+                if (xn < B && c0 + 24 <= a.cols && (a.cols & 7) == 0) {
+                    const __half* src = a.x + (int64_t)xn * a.cols + c0;
+                    *reinterpret_cast<uint4*>(&v[0]) = __ldg(reinterpret_cast<const uint4*>(src));
+                    *reinterpret_cast<uint4*>(&v[8]) = __ldg(reinterpret_cast<const uint4*>(src + 16));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = c0 + (j & 7) + (j >> 3) * 16;
+                        v[j] = (xn < B && col < a.cols) ? a.x[(int64_t)xn * a.cols + col] : __float2half(0.f);
+                    }
+                }
+                if constexpr (ASYM) {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sum += __half2float(v[j]);
+                    S.gsum[cp.sl & 1][xcb >> 2][xn][(xcb & 3) * 2 + xpt] = sum;
+                }
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {  // kappa = xcb*32 + 2j + h <- column j + 16h, j = 8xpt + 4cc + u
+                    uint32_t w[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        w[u] = (uint32_t)__half_as_ushort(v[4 * cc + u]) | ((uint32_t)__half_as_ushort(v[8 + 4 * cc + u]) << 16);
+                    const int jk = xcb * 4 + xpt * 2 + cc;
+                    *reinterpret_cast<uint4*>(xs + jk * 256 + (xn >> 3) * 128 + (xn & 7) * 16) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            {  // refill the weight ring with step st + kRing - 1
+                bool v = false;
+                const int nx = st + kRing - 1;
+                const uint4* src = nx < nsteps ? wsrc(wp, v) : a.planes;
+                cp16(&S.wring[nx % kRing][tid], src, nx < nsteps && v);
+                cp_async_commit();
+                advance(wp);
+            }
+            // scales of step st (converted and used by the epilogue of iteration st + 2)
+            sc_e = sc_1;
+            sc_1 = sc_2;
+            sc_2 = load_sc(sp, true);
+            advance(sp);
+            cp_async_wait<kRing - 1>();
+            const uint4 wv = S.wring[st % kRing][tid];
+            // un-rotate (stored byte j = row byte (j + r16) & 15) and expand
+            uint32_t o[4];
+            {
+                uint32_t w0 = wv.x, w1 = wv.y, w2 = wv.z, w3 = wv.w;
+                if (r16 & 8) {
+                    uint32_t t0 = w0, t1 = w1;
+                    w0 = w2; w1 = w3; w2 = t0; w3 = t1;
+                }
+                if (r16 & 4) {
+                    uint32_t tt = w3;
+                    w3 = w2; w2 = w1; w1 = w0; w0 = tt;
+                }
+                const int sh = 8 * (r16 & 3);
+                o[0] = __funnelshift_l(w3, w0, sh);
+                o[1] = __funnelshift_l(w0, w1, sh);
+                o[2] = __funnelshift_l(w1, w2, sh);
+                o[3] = __funnelshift_l(w2, w3, sh);
+            }
+            uint32_t h[32];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t nw = ~o[2 * kh + q];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) h[q * 16 + j] = ((nw << (15 - j)) & 0x80008000u) | 0x3C003C00u;
+            }
+            const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + 64 * slot + 32 * kh;
+            if (a.dbg != 32)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {"
+                "%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+                "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(h[8]),
+                "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(h[16]),
+                "r"(h[17]), "r"(h[18]), "r"(h[19]), "r"(h[20]), "r"(h[21]), "r"(h[22]), "r"(h[23]), "r"(h[24]),
+                "r"(h[25]), "r"(h[26]), "r"(h[27]), "r"(h[28]), "r"(h[29]), "r"(h[30]), "r"(h[31])
+                : "memory");
+            advance(cp);
+            if (st >= 2) epilogue(st - 2);  // (its scales: sc_e) -- overlaps the TMEM store
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            arrive(&S.a_full[slot]);
+        }
+        for (int e = nsteps - 2 < 0 ? 0 : nsteps - 2; e < nsteps; ++e) {
+            sc_e = sc_1;
+            sc_1 = sc_2;
+            epilogue(e);
+        }
+        cp_async_wait<0>();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kExp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
+    }
+}
+
 size_t gemm_workspace_bytes(const abcq_model_t* m, int B) {
     return (size_t)n_slices(m->cols) * B * n_row_tiles(m->rows) * kTileRows * sizeof(float);
 }
@@ -375,6 +745,21 @@ int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const vo
         a.set_of[b] = k < a.npset ? k : -1;
         if (a.set_of[b] < 0) a.overflow = 1;
     }
+    // the tcgen05 variant is opt-in (abcq_debug_set_mode(40)): correct, but
+    // measured slower than the mma.sync kernel on the 8B MLP
+    const bool use_tc = g_dbg_mode == 40 && !a.overflow;
+    a.dbg = 0;
+    auto go_tc = [&](auto kern) -> cudaError_t {
+        const int smem = (int)sizeof(tcg::Smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        const int n_items = (int)ceil_div(a.NRT, 8) * a.NS;
+        const int G = 2 * num_sms();
+        const int per = (int)ceil_div(n_items, G);
+        const int grid = (int)ceil_div(n_items, per);
+        kern<<<grid, tcg::kThreads, smem, st>>>(a, per);
+        return cudaGetLastError();
+    };
     const size_t smem = sizeof(GemmSmem);
     auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -393,7 +778,12 @@ int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const vo
         return cudaGetLastError();
     };
     cudaError_t e0;
-    if (m->scale_dtype == ABCQ_F16)
+    if (use_tc) {
+        if (m->scale_dtype == ABCQ_F16)
+            e0 = m->asymmetric ? go_tc(gemm_tc_kernel<__half, true>) : go_tc(gemm_tc_kernel<__half, false>);
+        else
+            e0 = m->asymmetric ? go_tc(gemm_tc_kernel<float, true>) : go_tc(gemm_tc_kernel<float, false>);
+    } else if (m->scale_dtype == ABCQ_F16)
         e0 = m->asymmetric ? go(gemm_mixedp_kernel<__half, true>) : go(gemm_mixedp_kernel<__half, false>);
     else
         e0 = m->asymmetric ? go(gemm_mixedp_kernel<float, true>) : go(gemm_mixedp_kernel<float, false>);

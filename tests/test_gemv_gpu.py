@@ -370,6 +370,35 @@ def test_gemm_mixedp_matches_per_request_oracle(P, rows, cols, asym):
             assert O.rel_dev(Y[b], want) <= 1e-4, (B, b, p, O.rel_dev(Y[b], want))
 
 
+@pytest.mark.parametrize("asym", [False, True])
+@pytest.mark.parametrize("scale_dtype", ["f16", "f32"])
+def test_gemm_mixedp_tcgen05_variant(P, asym, scale_dtype):
+    """The tcgen05 GEMM (A = expanded sign planes in tensor memory, B = X in
+    shared memory, D in tensor memory; opt-in debug mode 40) against the
+    per-request oracle, ragged rows/cols, B in {1, 7, 16}, p up to 6."""
+    from paper_2510_10467_b200 import _lib
+    rows, cols = 300, 1000
+    m = synth_model(P, rows, cols, 2, 6, asym=asym, seed=11)
+    dm = P.DeviceModel.from_model(m, scale_dtype=scale_dtype)
+    _lib.lib().abcq_debug_set_mode(40)
+    try:
+        for B in (1, 7, 16):
+            ps = [(2, 4, 6, 3)[b % 4] for b in range(B)]
+            X = np.stack([O.random_gaussian(1, cols, seed=300 + b).ravel() for b in range(B)])
+            Xh = X.astype(np.float16).astype(np.float32)
+            Y = dm.gemm_mixedp(ps, torch.from_numpy(Xh).cuda()).cpu().numpy()
+            for b, p in enumerate(ps):
+                a = m.scale_sets[p].alpha
+                z = m.scale_sets[p].offset
+                if scale_dtype == "f16":
+                    a = a.astype(np.float16).astype(np.float32)
+                    z = None if z is None else z.astype(np.float16).astype(np.float32)
+                want = O.gemv_lut(m.bitplanes.words, cols, 128, a, z, p, Xh[b])
+                assert O.rel_dev(Y[b], want) <= 1e-4, (B, b, p, O.rel_dev(Y[b], want))
+    finally:
+        _lib.lib().abcq_debug_set_mode(0)
+
+
 @pytest.mark.parametrize("scale_dtype", ["f16", "f32"])
 def test_gemm_mixedp_deep_precisions(P, scale_dtype):
     """p_max > 4 (planes staged in two rounds), more than kMaxSets distinct

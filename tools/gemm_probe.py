@@ -14,8 +14,11 @@ ap.add_argument("--rows", type=int, default=14336)
 ap.add_argument("--cols", type=int, default=4096)
 ap.add_argument("--B", type=int, default=16)
 ap.add_argument("--iters", type=int, default=50)
+ap.add_argument("--mode", type=int, default=0, help="abcq_debug_set_mode (30: the mma.sync kernel)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
+from paper_2510_10467_b200 import _lib  # noqa: E402
+_lib.lib().abcq_debug_set_mode(a.mode)
 gen = torch.Generator(device="cuda").manual_seed(0)
 dm = P.DeviceModel(a.rows, a.cols, 128, 2, 4, False, scale_dtype="f16")
 dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, a.rows, a.cols // 32), dtype=torch.int32, device=dev, generator=gen))

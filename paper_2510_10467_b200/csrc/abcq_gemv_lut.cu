@@ -14,7 +14,7 @@ unsigned long long* g_trace = nullptr;  // abcq_debug_set_trace (profiling aid)
 int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experiments)
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
-int g_piece_blocks = 200;
+int g_piece_blocks = 0;  // 0: by batch size (below)
 int g_partition = 0;  // 0: greedy fill with exact piece costs; 1: proportional (abcq_debug_set_mode(3000 + v))
 int g_prefill = 8;  // ring slots issued before the PDL wait (all of them); abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
@@ -73,6 +73,10 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                      int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st) {
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
+    // fixed cost of a (job, slice) piece in blocks: measured best 200 for
+    // single GEMVs and decoder-sized groups, 130-160 for large batches (bench
+    // step 60.4 -> 59.6 us; tools/ab_step.py / ab_small.py with modes 1xxx)
+    const int piece_blocks = g_piece_blocks > 0 ? g_piece_blocks : (n >= 8 ? 150 : 200);
     char* w = static_cast<char*>(ws);
     int items = 0;
     int64_t units = 0;
@@ -87,7 +91,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
         Job& J = a.jobs[j];
         J.ibase = items;
         J.ubase = units;
-        J.w = kCostScale * ps[j] + (int)ceil_div((int64_t)kCostScale * g_piece_blocks, J.NRT);
+        J.w = kCostScale * ps[j] + (int)ceil_div((int64_t)kCostScale * piece_blocks, J.NRT);
         items += J.items;
         units += (int64_t)J.items * J.w;
     }
@@ -107,7 +111,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     auto put = [&](int v) { key.append(reinterpret_cast<const char*>(&v), sizeof(v)); };
     put(grid);
     put(g_partition);
-    put(g_piece_blocks);
+    put(piece_blocks);
     for (int j = 0; j < n; ++j) {
         put(a.jobs[j].rows);
         put(a.jobs[j].cols);
@@ -136,7 +140,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                     const Job& J = a.jobs[j];
                     const int loc = g - J.ibase, s = loc / J.NRT;
                     const int pend = J.ibase + (s + 1) * J.NRT;  // end of this piece
-                    const int64_t start = (int64_t)g_piece_blocks * 64;
+                    const int64_t start = (int64_t)piece_blocks * 64;
                     const int64_t per = (int64_t)J.p * 64;
                     if (cost > 0 && cost + start + per > T) break;  // next CTA takes this piece
                     cost += start;
@@ -151,7 +155,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             if (write) a.cta_it[grid] = g;
             return g >= items;
         };
-        int64_t lo = 1, hi = (int64_t)64 * (units / 64 + 1) + (int64_t)64 * g_piece_blocks * 4 * (items + 1);
+        int64_t lo = 1, hi = (int64_t)64 * (units / 64 + 1) + (int64_t)64 * piece_blocks * 4 * (items + 1);
         while (lo < hi) {
             const int64_t mid = lo + (hi - lo) / 2;
             if (fill(mid, false)) hi = mid;

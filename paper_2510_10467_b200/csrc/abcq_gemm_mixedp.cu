@@ -379,10 +379,22 @@ constexpr uint32_t kDCol = 64 * kSlots;
 constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);  // f16.f16->f32
 constexpr int kXBytes = kN * 256 * 2;     // one slice of X (16 requests x 256 columns, f16)
 constexpr int kRing = 8;                  // weight steps in flight per thread (cp.async)
+constexpr int kMaxSteps = 768;            // per CTA (step descriptors in shared memory)
+// one (group, plane) step of a CTA, precomputed once: the per-step work is then
+// a broadcast load plus the thread's constant offsets (no divisions, no cursors)
+struct StepDesc {
+    uint32_t w;       // plane word (uint4) index of the step's first row: i*pst + (sl*NRT + tile0)*32 + gl*16
+    uint32_t s;       // scale element index of the step's first row: i*items*32 + (sl*NRT + tile0)*32 + gl*16
+    uint32_t sl;      // slice
+    uint16_t tile0;   // first row tile of the 128-row block
+    uint8_t i;        // plane
+    uint8_t f;        // bit 0 gl, 1 new slice (stage X), 2 item end (store partials), 3 X buffer, 4..7 valid tiles (0..8)
+};
 struct Smem {
     char x[2][kXBytes];                   // X of a slice, core-matrix layout; slice parity picks the buffer
     uint4 wring[kRing][kExp * 32];        // per-thread weight ring
     float gsum[2][2][kN][8];              // asymmetric: [xbuf][group][request][16-col part] sums of x
+    StepDesc desc[kMaxSteps];
     uint64_t a_full[kSlots], d_full[kSlots], d_empty[kSlots];
     uint32_t tmem;
 };
@@ -415,6 +427,22 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
     const int spi = 2 * a.pmax;  // steps per item: group-major, plane-minor
     const int nsteps = it1 > it0 ? (it1 - it0) * spi : 0;
 
+    // step descriptors (all threads; one division chain per step, once)
+    for (int st = tid; st < nsteps; st += kThreads) {
+        const int item = st / spi, r = st - item * spi, gl = r / a.pmax, i = r - gl * a.pmax;
+        const int it = it0 + item, sl = it / NRB, rb = it - sl * NRB, tile0 = rb * 8;
+        const uint32_t rowbase = (uint32_t)(sl * a.NRT + tile0) * 32 + gl * 16;
+        StepDesc d;
+        d.w = (uint32_t)(i * a.plane_stride_u4) + rowbase;
+        d.s = (uint32_t)i * (uint32_t)a.items * 32 + rowbase;
+        d.sl = sl;
+        d.tile0 = (uint16_t)tile0;
+        d.i = (uint8_t)i;
+        const bool newsl = r == 0 && (item == 0 || rb == 0);
+        const int nt = min(8, a.NRT - tile0);
+        d.f = (uint8_t)(gl | (newsl ? 2 : 0) | (r == spi - 1 ? 4 : 0) | ((sl & 1) << 3) | (nt << 4));
+        S.desc[st] = d;
+    }
     if (warp == kExp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&S.tmem)),
                      "n"(kTmemCols)
@@ -437,20 +465,16 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
     if (warp == kExp) {
         // ---- MMA issuer -------------------------------------------------------
         if (lane == 0) {
+            const uint32_t x0 = smem_addr(S.x[0]);
             for (int st = 0; st < nsteps; ++st) {
                 const int slot = st % kSlots;
                 const uint32_t ph = (st / kSlots) & 1;
+                const uint32_t f = S.desc[st].f;
                 mbar_wait(&S.a_full[slot], ph);
                 if (st >= kSlots) mbar_wait(&S.d_empty[slot], ph ^ 1);  // epilogue of step st - kSlots
                 tc_fence_after();
-                const int it = it0 + st / spi, r = st % spi, gl = r / a.pmax;
-                const int sl = it / NRB;
-                const uint32_t xaddr = smem_addr(S.x[sl & 1]) + gl * 8 * 512;
+                const uint32_t xaddr = x0 + ((f >> 3) & 1) * kXBytes + (f & 1) * 8 * 512;
                 const uint32_t d_t = tbase + kDCol + 16 * slot, a_t = tbase + 64 * slot;
-                if (a.dbg == 31) {
-                    arrive(&S.d_full[slot]);
-                    continue;
-                }
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t bd = bdesc(xaddr + kk * 512);
@@ -467,107 +491,78 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
             }
         }
     } else {
-        // ---- expanders / epilogue: thread t = row t of the 128-row block ---------
+        // ---- expanders / epilogue ----------------------------------------------
         // thread = (row t of the 128-row block, K half kh): warps w and w+4 share
         // TMEM lane quarter w; kh picks 64 of the group's 128 columns (A columns
         // [32kh, 32kh+32) of a slot) and 8 of the 16 requests in the epilogue
         const int kh = warp >> 2, t = (warp & 3) * 32 + lane, r16 = t & 15, tib = t >> 4;
+        const uint32_t toff = (uint32_t)tib * 32 + r16;  // the thread's row inside a step's block
         const int B = a.B;
         const int64_t NRT16 = (int64_t)a.NRT * kTileRows;
-        const int64_t pst = a.plane_stride_u4;
         constexpr int kNh = kN / 2;  // requests per thread: kh*8 .. kh*8+7
         int sb[kNh];
 #pragma unroll
         for (int b = 0; b < kNh; ++b) sb[b] = kh * kNh + b < B ? a.set_of[kh * kNh + b] : 0;
-        // step cursors (no divisions in the loop): item it = (slice sl, row block
-        // rb), group gl of the slice, plane i; steps run group-major, plane-minor
-        struct Pos {
-            int it, sl, rb, gl, i;
-        };
-        auto pos_at = [&](int st) {
-            Pos q;
-            const int item = st / spi, r = st - item * spi;
-            q.it = it0 + item;
-            q.sl = q.it / NRB;
-            q.rb = q.it - q.sl * NRB;
-            q.gl = r / a.pmax;
-            q.i = r - q.gl * a.pmax;
-            return q;
-        };
-        auto advance = [&](Pos& q) {
-            if (++q.i < a.pmax) return;
-            q.i = 0;
-            if (++q.gl < 2) return;
-            q.gl = 0;
-            ++q.it;
-            if (++q.rb == NRB) {
-                q.rb = 0;
-                ++q.sl;
-            }
-        };
-        // raw (unconverted) scales of a step: one per staged precision set; the
-        // conversion happens at the epilogue, two steps later, so the loads are
-        // never waited on in the step that issues them
+        const ST* alp[kMaxSets];
+        const ST* zp[kMaxSets];
+        int pk[kMaxSets];
+#pragma unroll
+        for (int k = 0; k < kMaxSets; ++k) {
+            pk[k] = k < a.npset ? a.pset[k] : 0;
+            alp[k] = static_cast<const ST*>(a.alpha[pk[k]]);
+            zp[k] = ASYM ? static_cast<const ST*>(a.offset[pk[k]]) : nullptr;
+        }
         struct Sc {
             ST al[kMaxSets];
             ST z[kMaxSets];
         };
         const ST zero = from_f32<ST>(0.f);
-        auto load_sc = [&](const Pos& q, bool live) {
+        auto load_sc = [&](const StepDesc& d) {  // raw scales of a step (converted two steps later)
             Sc c;
-            const int tile = min(q.rb * 8 + tib, a.NRT - 1);
-            const int64_t e = (int64_t)(q.sl * a.NRT + tile) * 32 + q.gl * 16 + r16;
+            const uint32_t e = d.s + toff;
 #pragma unroll
             for (int k = 0; k < kMaxSets; ++k) {
-                const int pk = k < a.npset ? a.pset[k] : 0;
-                c.al[k] = (live && q.i < pk) ? __ldg(static_cast<const ST*>(a.alpha[pk]) + (int64_t)q.i * a.items * 32 + e)
-                                             : zero;
-                if constexpr (ASYM)
-                    c.z[k] = (live && q.i == 0 && pk > 0) ? __ldg(static_cast<const ST*>(a.offset[pk]) + e) : zero;
-                else
-                    c.z[k] = zero;
+                c.al[k] = d.i < pk[k] ? __ldg(alp[k] + e) : zero;
+                if constexpr (ASYM) c.z[k] = (d.i == 0 && pk[k] > 0) ? __ldg(zp[k] + e) : zero;
+                else c.z[k] = zero;
             }
             return c;
         };
-        auto wsrc = [&](const Pos& q, bool& valid) -> const uint4* {
-            const int tile = q.rb * 8 + tib;
-            valid = tile < a.NRT;
-            return a.planes + q.i * pst + ((int64_t)(q.sl * a.NRT + (valid ? tile : 0)) * 32 + q.gl * 16 + r16);
-        };
-        Pos wp = pos_at(0), cp = wp, sp = wp, ep = wp;
-        // prologue: weight ring (steps 0 .. kRing-2), scales of step 0
-        for (int k = 0; k < kRing - 1; ++k) {
+        auto refill = [&](int nx) {  // weight ring slot of step nx
             bool v = false;
-            const uint4* src = k < nsteps ? wsrc(wp, v) : a.planes;
-            cp16(&S.wring[k][tid], src, k < nsteps && v);
+            const uint4* src = a.planes;
+            if (nx < nsteps) {
+                const StepDesc d = S.desc[nx];
+                v = tib < (d.f >> 4);
+                src = a.planes + (v ? d.w + toff : 0u);
+            }
+            cp16(&S.wring[nx % kRing][tid], src, v);
             cp_async_commit();
-            advance(wp);
-        }
+        };
+        for (int k = 0; k < kRing - 1; ++k) refill(k);
         Sc sc_e, sc_1, sc_2;  // after iteration st's rotation: scales of steps st-2 (epilogue), st-1, st
         float acc[kNh];
 #pragma unroll
         for (int b = 0; b < kNh; ++b) acc[b] = 0.f;
-        int staged = -1;
         // X staging: request xn, 32-column block xcb, half xpt (kappa chunks 2xpt, 2xpt+1)
         const int xn = tid >> 4, xcb = (tid >> 1) & 7, xpt = tid & 1;
 
         auto epilogue = [&](int e) {
             const int slot = e % kSlots;
+            const StepDesc d = S.desc[e];
             mbar_wait(&S.d_full[slot], (e / kSlots) & 1);
             tc_fence_after();
-            uint32_t d[8] = {};
-            if (a.dbg != 33)
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
-                : "r"(tbase + ((uint32_t)((warp & 3) * 32) << 16) + kDCol + 16 * slot + 8 * kh)
-                : "memory");
+            uint32_t dv[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(dv[0]), "=r"(dv[1]), "=r"(dv[2]), "=r"(dv[3]), "=r"(dv[4]), "=r"(dv[5]), "=r"(dv[6]),
+                           "=r"(dv[7])
+                         : "r"(tbase + ((uint32_t)((warp & 3) * 32) << 16) + kDCol + 16 * slot + 8 * kh)
+                         : "memory");
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
             arrive(&S.d_empty[slot]);
-            // per-request coefficient: alpha of the request's precision set (already 0
-            // where the set's precision <= i); scalar selects, no indexed array (an
-            // indexed register array is spilled to local memory)
+            // per-request coefficient: alpha of the request's precision set (0 where
+            // the set's precision <= i); scalar selects, no indexed register array
             static_assert(kMaxSets == 4, "four scale sets");
             const float a0 = to_f32<ST>(sc_e.al[0]), a1 = to_f32<ST>(sc_e.al[1]);
             const float a2 = to_f32<ST>(sc_e.al[2]), a3 = to_f32<ST>(sc_e.al[3]);
@@ -575,15 +570,15 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
             for (int b = 0; b < kNh; ++b) {
                 const int k = sb[b];
                 const float c = k < 2 ? (k == 0 ? a0 : a1) : (k == 2 ? a2 : a3);
-                acc[b] = fmaf(c, __uint_as_float(d[b]), acc[b]);
+                acc[b] = fmaf(c, __uint_as_float(dv[b]), acc[b]);
             }
             if constexpr (ASYM) {
-                if (ep.i == 0) {
+                if (d.i == 0) {
                     const float z0 = to_f32<ST>(sc_e.z[0]), z1 = to_f32<ST>(sc_e.z[1]);
                     const float z2 = to_f32<ST>(sc_e.z[2]), z3 = to_f32<ST>(sc_e.z[3]);
 #pragma unroll
                     for (int b = 0; b < kNh; ++b) {
-                        const float* gs = S.gsum[ep.sl & 1][ep.gl][kh * kNh + b];
+                        const float* gs = S.gsum[(d.f >> 3) & 1][d.f & 1][kh * kNh + b];
                         const float gx = ((gs[0] + gs[1]) + (gs[2] + gs[3])) + ((gs[4] + gs[5]) + (gs[6] + gs[7]));
                         const int k = sb[b];
                         const float z = k < 2 ? (k == 0 ? z0 : z1) : (k == 2 ? z2 : z3);
@@ -591,10 +586,9 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
                     }
                 }
             }
-            if (ep.gl == 1 && ep.i == a.pmax - 1) {  // item done: this row's partial for the slice
-                const int tile = ep.rb * 8 + tib;
-                if (tile < a.NRT) {
-                    float* out = a.partial + ((int64_t)ep.sl * B + kh * kNh) * NRT16 + tile * kTileRows + r16;
+            if (d.f & 4) {  // item done: this row's partial for the slice
+                if (tib < (d.f >> 4)) {
+                    float* out = a.partial + ((int64_t)d.sl * B + kh * kNh) * NRT16 + (d.tile0 + tib) * kTileRows + r16;
 #pragma unroll
                     for (int b = 0; b < kNh; ++b)
                         if (kh * kNh + b < B) out[b * NRT16] = acc[b];
@@ -602,15 +596,14 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
 #pragma unroll
                 for (int b = 0; b < kNh; ++b) acc[b] = 0.f;
             }
-            advance(ep);
         };
 
         for (int st = 0; st < nsteps; ++st) {
             const int slot = st % kSlots;
-            if (cp.gl == 0 && cp.i == 0 && cp.sl != staged) {  // stage X of this slice (B operand), permuted K order
-                staged = cp.sl;
-                char* xs = S.x[cp.sl & 1];
-                const int c0 = cp.sl * 256 + xcb * 32 + xpt * 8;  // columns c0 + [0,8) and c0 + 16 + [0,8)
+            const StepDesc d = S.desc[st];
+            if (d.f & 2) {  // stage X of this slice (B operand), permuted K order
+                char* xs = S.x[(d.f >> 3) & 1];
+                const int c0 = d.sl * 256 + xcb * 32 + xpt * 8;  // columns c0 + [0,8) and c0 + 16 + [0,8)
                 __half v[16];
                 if (xn < B && c0 + 24 <= a.cols && (a.cols & 7) == 0) {
                     const __half* src = a.x + (int64_t)xn * a.cols + c0;
@@ -627,7 +620,7 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
                     float sum = 0.f;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) sum += __half2float(v[j]);
-                    S.gsum[cp.sl & 1][xcb >> 2][xn][(xcb & 3) * 2 + xpt] = sum;
+                    S.gsum[(d.f >> 3) & 1][xcb >> 2][xn][(xcb & 3) * 2 + xpt] = sum;
                 }
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {  // kappa = xcb*32 + 2j + h <- column j + 16h, j = 8xpt + 4cc + u
@@ -641,22 +634,13 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
-            {  // refill the weight ring with step st + kRing - 1
-                bool v = false;
-                const int nx = st + kRing - 1;
-                const uint4* src = nx < nsteps ? wsrc(wp, v) : a.planes;
-                cp16(&S.wring[nx % kRing][tid], src, nx < nsteps && v);
-                cp_async_commit();
-                advance(wp);
-            }
-            // scales of step st (converted and used by the epilogue of iteration st + 2)
+            refill(st + kRing - 1);
             sc_e = sc_1;
             sc_1 = sc_2;
-            sc_2 = load_sc(sp, true);
-            advance(sp);
+            sc_2 = load_sc(d);
             cp_async_wait<kRing - 1>();
             const uint4 wv = S.wring[st % kRing][tid];
-            // un-rotate (stored byte j = row byte (j + r16) & 15) and expand
+            // un-rotate (stored byte j = row byte (j + r16) & 15) and expand this K half
             uint32_t o[4];
             {
                 uint32_t w0 = wv.x, w1 = wv.y, w2 = wv.z, w3 = wv.w;
@@ -677,12 +661,11 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
             uint32_t h[32];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                const uint32_t nw = ~o[2 * kh + q];
+                const uint32_t nw = ~(kh ? o[2 + q] : o[q]);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) h[q * 16 + j] = ((nw << (15 - j)) & 0x80008000u) | 0x3C003C00u;
             }
             const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + 64 * slot + 32 * kh;
-            if (a.dbg != 32)
             asm volatile(
                 "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {"
                 "%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -692,7 +675,6 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
                 "r"(h[17]), "r"(h[18]), "r"(h[19]), "r"(h[20]), "r"(h[21]), "r"(h[22]), "r"(h[23]), "r"(h[24]),
                 "r"(h[25]), "r"(h[26]), "r"(h[27]), "r"(h[28]), "r"(h[29]), "r"(h[30]), "r"(h[31])
                 : "memory");
-            advance(cp);
             if (st >= 2) epilogue(st - 2);  // (its scales: sc_e) -- overlaps the TMEM store
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -755,7 +737,9 @@ int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const vo
         if (e != cudaSuccess) return e;
         const int n_items = (int)ceil_div(a.NRT, 8) * a.NS;
         const int G = 2 * num_sms();
-        const int per = (int)ceil_div(n_items, G);
+        int per = (int)ceil_div(n_items, G);
+        const int cap = tcg::kMaxSteps / (2 * a.pmax);  // step descriptors per CTA
+        if (per > cap) per = cap;
         const int grid = (int)ceil_div(n_items, per);
         kern<<<grid, tcg::kThreads, smem, st>>>(a, per);
         return cudaGetLastError();

@@ -200,7 +200,7 @@ constexpr int kReduceRows = kReduceThreads / kReduceTPR * kReduceRPT;  // rows p
 // RELEASE: let the dependent grid launch once this block's job has arrived --
 // not earlier, or the next kernel's CTAs take the SMs that the remaining
 // reduce blocks of this grid still need.
-template <int NJ, typename YT, int RPB, int RPT, bool RELEASE>
+template <int NJ, typename YT, int RPB, int RPT, bool RELEASE, bool PRE_WAIT = false>
 __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     constexpr int rpb = RPB;
     int j = 0, nbj = 0;
@@ -212,10 +212,12 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         blk -= nbj;
     }
     if (j >= a.n_jobs) {
+        if (PRE_WAIT) pdl_wait();
         if (RELEASE) pdl_launch_dependents();
         return;
     }
     const Job& J = a.jobs[j];
+    if (PRE_WAIT) pdl_wait();  // (after the param-space job scan: y may still be read by the previous kernel)
     // wait for this job's CTA arrivals only (acquire), so the reduction
     // overlaps the GEMV CTAs still streaming other jobs
     if (threadIdx.x == 0) {
@@ -306,8 +308,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             // retire) -- for batches whose reduce fits one wave; larger ones
             // use the separate kernel (a trailing CTA needs a whole SM, and
             // the role's code in the kernel costs the streams ~7%)
-            pdl_wait();  // (y may still be read by the previous kernel)
-            reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true>(a, blockIdx.x - a.main_ctas);
+            reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true, true>(a, blockIdx.x - a.main_ctas);
             return;
         }
     }
@@ -430,10 +431,30 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         issue(ic, s_fill);
         advance(ic);
     }
-    pdl_wait();  // x, y and the workspace belong to the previous kernel
-    pdl_launch_dependents();
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
-
+    // everything that reads only parameters / shared memory happens before the
+    // PDL wait too: the first two rounds' pieces and x addresses, the lookup
+    // column registers (param-space loads miss the constant cache at kernel start)
+    const bool has0 = it0 < it1;
+    Round R0, R1;
+    bool has1 = false;
+    const XT* xp0 = nullptr;
+    const XT* xp1 = nullptr;
+    int xk0 = 0, xk1 = 0, xc0 = 0, xc1 = 0;
+    if (has0) {
+        R0 = make_round(a, it0, it1);
+        const Job& J0 = a.jobs[R0.pc[0].j];
+        xp0 = static_cast<const XT*>(J0.x);
+        xk0 = R0.pc[0].s * kSliceCols + 8 * (tid & 31);
+        xc0 = J0.cols;
+        has1 = R0.end < it1;
+        if (has1) {
+            R1 = make_round(a, R0.end, it1);
+            const Job& J1 = a.jobs[R1.pc[0].j];
+            xp1 = static_cast<const XT*>(J1.x);
+            xk1 = R1.pc[0].s * kSliceCols + 8 * (tid & 31);
+            xc1 = J1.cols;
+        }
+    }
     const int half = lane >> 4, r = lane & 15;
     uint32_t rb[6];
 #pragma unroll
@@ -474,20 +495,13 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
 
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
     int round = 0;
+    pdl_wait();  // x, y and the workspace belong to the previous kernel
+    pdl_launch_dependents();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
     {
         float xv0[8], xv1[8];
-        const bool has0 = it0 < it1;
-        Round R0, R1;
-        bool has1 = false;
-        if (has0) {
-            R0 = make_round(a, it0, it1);
-            piece_x(R0, tid & 31, xv0);
-            has1 = R0.end < it1;
-            if (has1) {
-                R1 = make_round(a, R0.end, it1);
-                piece_x(R1, tid & 31, xv1);
-            }
-        }
+        if (has0) load_x8<XT>(xp0, xk0, xc0, xv0);
+        if (has1) load_x8<XT>(xp1, xk1, xc1, xv1);
         for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
             issue(ic, s_fill);
             advance(ic);

@@ -73,10 +73,10 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                      int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st) {
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
-    // fixed cost of a (job, slice) piece in blocks: measured best 200 for
+    // fixed cost of a (job, slice) piece in blocks: measured best 300 for
     // single GEMVs and decoder-sized groups, 130-160 for large batches (bench
     // step 60.4 -> 59.6 us; tools/ab_step.py / ab_small.py with modes 1xxx)
-    const int piece_blocks = g_piece_blocks > 0 ? g_piece_blocks : (n >= 8 ? 150 : 200);
+    const int piece_blocks = g_piece_blocks > 0 ? g_piece_blocks : (n >= 8 ? 150 : 300);
     char* w = static_cast<char*>(ws);
     int items = 0;
     int64_t units = 0;

@@ -340,6 +340,43 @@ def test_gemv_batch_plan_repeated_launches(P):
         P.GemvBatchPlan([(models[0], 5, x, jobs[0][3])])  # precision outside [p_lo, p_hi]
 
 
+def test_gemv_batch_more_jobs_than_one_launch(P):
+    """40 jobs (> abcq_gemv_batch_max_jobs) split over two launches == single calls, bitwise."""
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.device_model import gemv_batch
+    assert _lib.lib().abcq_gemv_batch_max_jobs() < 40
+    dms = [P.DeviceModel.from_model(synth_model(P, r, 512, 2, 4, seed=r), scale_dtype="f16") for r in (64, 200, 1000)]
+    x = torch.from_numpy(O.random_gaussian(1, 512, seed=9).ravel()).cuda().half()
+    jobs = [(dms[k % 3], 2 + k % 3, x, torch.empty(dms[k % 3].rows, device="cuda", dtype=torch.float16))
+            for k in range(40)]
+    gemv_batch(jobs)
+    torch.cuda.synchronize()
+    for dm, p, _, out in jobs:
+        assert torch.equal(out, dm.gemv(p, x, out_dtype=torch.float16))
+
+
+def test_split_k_completion_paths_agree(P):
+    """Trailing-CTA completion (one launch) and the standalone PDL-chained
+    reduce kernel (debug mode 22) give bitwise-identical y (fixed chain order)."""
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.device_model import gemv_batch
+    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r + c), scale_dtype="f16")
+           for r, c in ((4096, 4096), (1024, 14336), (300, 1000))]
+    x = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for c in (4096, 14336, 1000)}
+    jobs = [(dm, p, x[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16)) for dm in dms for p in (2, 4)]
+    gemv_batch(jobs)
+    torch.cuda.synchronize()
+    fused = [o.clone() for *_, o in jobs]
+    _lib.lib().abcq_debug_set_mode(22)
+    try:
+        gemv_batch(jobs)
+        torch.cuda.synchronize()
+    finally:
+        _lib.lib().abcq_debug_set_mode(0)
+    for (*_, o), f in zip(jobs, fused):
+        assert torch.equal(o, f)
+
+
 def test_gemv_batch_asymmetric(P):
     from paper_2510_10467_b200.device_model import gemv_batch
     ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]

@@ -291,10 +291,13 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     }
 }
 
-// profiling stamps (abcq_debug_set_trace): per CTA, slot k = max over the
-// calling warps of %globaltimer. 0 start, 1 after the PDL wait, 2 first table
-// ready, 3 streams done, 4 / 5 first / last warp done with round 0, 6 =
-// rounds, 7 round-1 table ready
+// profiling stamps (abcq_debug_set_trace; tools/layer_probe.py reads them):
+// per CTA (8 slots of %globaltimer) 0 start, 1 release fence done, 2 first
+// table ready, 3 streams done (max over warps), 4 arrivals issued, 5 all
+// warps done, 6 = rounds, 7 past the PDL wait; per job (rows 149 / 156 / 160
+// / 164 of the launch's slot): last row reduced, last reduce block started,
+// last CTA arrival, last reduce block past its wait; row 148: reduce grid
+// first start / first wait passed / end
 #define ABCQ_BTRACE(k)                                                                   \
     do {                                                                                 \
         if (a.trace && lane == 0) atomicMax(&a.trace[blockIdx.x * 8 + (k)], globaltimer()); \

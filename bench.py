@@ -363,6 +363,32 @@ def run_gpu(args):
         del pool, fused_w
         del dense
 
+    # ---- per shape, launch latency amortised: one gemv_batch of 8 independent
+    # same-shape GEMVs (8 distinct weight sets, e.g. 8 adapters / requests on
+    # different models), back to back over 2 such groups (> 2x L2 for the big
+    # shapes; the small ones are partly L2-resident -- reported as measured)
+    per_shape_b8 = {}
+    if rank == 0 and not args.no_cpu:
+        peak8, _ = read_peaks()
+        for li, (name, r, k) in enumerate(LAYERS):
+            if name in ("k", "v", "o", "up"):  # same shapes as q / gate
+                continue
+            pool8 = []
+            for c in range(16):
+                dm = P.DeviceModel(r, k, 128, P_LO, P_HI, False, scale_dtype="f16")
+                dm.load_planes(torch.randint(-2**31, 2**31 - 1, (P_HI, r, k // 32), dtype=torch.int32, device=dev))
+                for pp in PRECISIONS:
+                    dm.load_scale_set(pp, 0.01 + 0.1 * torch.rand(pp, r, k // 128, device=dev))
+                pool8.append(dm)
+            yb = [torch.empty(r, dtype=torch.float16, device=dev) for _ in range(16)]
+            for pp in PRECISIONS:
+                us = 1e3 * time_graph(lambda: [gemv_batch([(pool8[8 * h + j], pp, xs[k], yb[8 * h + j]) for j in range(8)],
+                                                          stream) for h in range(2)], reps=10) / 2
+                gbps = 8 * algo_bytes(r, k, pp) / (us * 1e-6) / 1e9
+                per_shape_b8[f"{name}_{r}x{k}_p{pp}"] = {"us_per_launch": round(us, 2), "GBps": round(gbps, 1),
+                                                         "roofline_frac": round(gbps / peak8, 4)}
+            del pool8, yb
+
     # ---- e2e: public API with pinned host buffers, copies in the timed region
     e2e = None
     if rank == 0:
@@ -478,6 +504,10 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "per_shape": per_shape,
+            "per_shape_batched8": per_shape_b8,
+            "per_shape_batched8_note": "one gemv_batch of 8 independent same-shape GEMVs (distinct weights) per "
+                                       "launch, back to back: the per-shape kernel rate with the launch latency "
+                                       "amortised",
             "per_shape_note": "single launches, graph of 20 back-to-back launches rotating 3 weight copies "
                               "(the smaller layers can be partly L2-resident)",
             "fp16_cublas": fp16,

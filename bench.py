@@ -188,29 +188,55 @@ def run_gpu(args):
     models = make_layer_models(P, 1, copies, seed0=17 * rank)
     xs = {k: (torch.randn(k, device=dev) * 1.0).half() for k in {c for _, _, c in LAYERS}}
     ys = [[torch.empty(m.rows, dtype=torch.float16, device=dev) for m in row] for row in models]
-    gathered = None
-    if world > 1:
-        gathered = [[torch.empty(m.rows * world, dtype=torch.float16, device=dev) for m in row] for row in models]
+    # multi-GPU step: the 21 row-sharded outputs of a step live in ONE flat
+    # buffer, all-gathered by ONE NCCL call that overlaps the next step's
+    # GEMV launch (two buffer sets; a step waits only for the gather that last
+    # read its buffer)
+    mp = world > 1 or os.environ.get("ABCQ_BENCH_FORCE_MP") == "1"
+    if mp and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
 
     stream = torch.cuda.Stream(device=dev)
 
     from paper_2510_10467_b200.device_model import gemv_batch
 
-    def grouped_launches(groups):
+    def grouped_launches(groups):  # (rank 0 only: local launches, no collectives)
         for pi, p in enumerate(PRECISIONS):
             for grp in groups:
                 gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
-                if world > 1:
-                    for li in grp:
-                        dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
 
     all_jobs = [(pi, p, li) for pi, p in enumerate(PRECISIONS) for li in range(len(LAYERS))]
 
-    def step_launches():
+    def step_launches():  # single GPU (multi-GPU: step_mp)
         gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for pi, p, li in all_jobs], stream)
-        if world > 1:
+
+    mp_rows = sum(models[pi][li].rows for pi, p, li in all_jobs)
+    mp_y = [torch.empty(mp_rows, dtype=torch.float16, device=dev) for _ in range(2)] if mp else None
+    mp_g = [torch.empty(mp_rows * world, dtype=torch.float16, device=dev) for _ in range(2)] if mp else None
+    mp_views = []
+    if mp:
+        for b in range(2):
+            off, v = 0, []
             for pi, p, li in all_jobs:
-                dist.all_gather_into_tensor(gathered[pi][li], ys[pi][li])
+                v.append(mp_y[b][off:off + models[pi][li].rows])
+                off += models[pi][li].rows
+            mp_views.append(v)
+    mp_work = [None, None]
+    mp_plan = [P.GemvBatchPlan([(models[pi][li], p, xs[models[pi][li].cols], mp_views[b][n])
+                                for n, (pi, p, li) in enumerate(all_jobs)]) for b in range(2)] if mp else None
+
+    def step_mp(i):
+        b = i & 1
+        if mp_work[b] is not None:
+            mp_work[b].wait()  # (stream waits for the gather that last read mp_y[b])
+        mp_plan[b].launch(stream)
+        mp_work[b] = dist.all_gather_into_tensor(mp_g[b], mp_y[b], async_op=True)
+
+    def mp_drain():
+        for b in range(2):
+            if mp_work[b] is not None:
+                mp_work[b].wait()
+                mp_work[b] = None
 
     def single_launches():
         for pi, p in enumerate(PRECISIONS):
@@ -239,10 +265,12 @@ def run_gpu(args):
     # as CUDA graphs of up to 50 consecutive steps each (a graph per step would
     # leave a replay gap between steps)
     with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):
-            step_launches()
+        for i in range(max(args.warmup, 3)):
+            step_mp(i) if mp else step_launches()
+        if mp:
+            mp_drain()
     torch.cuda.synchronize()
-    use_graph = world == 1
+    use_graph = not mp
     plan = []  # (graph, steps in it), replayed in order: exactly K steps
     if use_graph:
         per = min(args.steps, 50)
@@ -264,7 +292,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     # ---- timed region: K steps, events on the launching stream ------------
-    if world > 1:
+    if mp:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -277,13 +305,14 @@ def run_gpu(args):
                 for g, _ in plan:
                     g.replay()
             else:
-                for _ in range(args.steps):
-                    step_launches()
+                for i in range(args.steps):
+                    step_mp(i)
+                mp_drain()  # the last steps' gathers complete inside the timed region
             ev1.record(stream)
         torch.cuda.synchronize()
         clk.mark(False)
     ms = ev0.elapsed_time(ev1)
-    if world > 1:
+    if mp:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -491,10 +520,12 @@ def run_gpu(args):
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
                              f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
-                       "timing": "the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream",
+                       "timing": ("the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream"
+                                  if not mp else "eager steps, one NCCL all-gather of the step's 21 outputs per "
+                                  "step overlapping the next step (double-buffered), CUDA events, max over ranks"),
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
             # per step: the persistent batched GEMV kernel + the split-K reduce kernel
-            "gpu_launches": args.steps * 2,
+            "gpu_launches": args.steps * 2,  # (+ one NCCL all-gather per step when multi-GPU)
             "step_variants": variants,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -513,7 +544,7 @@ def run_gpu(args):
             "fp16_cublas": fp16,
         }
         print(json.dumps(line))
-    if world > 1:
+    if mp:
         dist.destroy_process_group()
 
 

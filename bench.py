@@ -53,6 +53,9 @@ P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
 XY_BYTES = 2      # fp16 x and y
 METRIC = "bit-plane GEMV HBM GB/s (Llama-3-8B layer sweep, p=2/3/4, batch 1)"
+WORKLOAD = ("Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, p=2,3,4 per step, g=128, fp16 "
+            "scales/x/y; the 21 independent GEMVs (per-request precision) run as one persistent "
+            "mixed-precision batched launch + one split-K reduce launch")
 
 
 def algo_bytes(rows: int, cols: int, p: int) -> int:
@@ -512,10 +515,7 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
-            "config": {"workload": "Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, "
-                                   "p=2,3,4 per step, g=128, fp16 scales/x/y; the 21 independent GEMVs "
-                                   "(per-request precision) run as one persistent mixed-precision "
-                                   "batched launch + one split-K reduce launch",
+            "config": {"workload": WORKLOAD,
                        "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
                        "bytes_per_step": kernel_bytes,
                        "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
@@ -609,10 +609,12 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     value = round(step_bytes() / dt / 1e9, 3)
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": {"workload": "Llama-3-8B layer sweep GEMV, batch 1, p=2,3,4"},
+        "data": "synthetic", "config": {"workload": WORKLOAD, "implementation": "reference CPU algorithm "
+                                        "(C restatement of GemvEngine.lut, all host threads)"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": "full layer sweep per step (C restatement of GemvEngine.lut; "
                                    "reference is Python+numba, no compiled sources to build)"},

@@ -306,20 +306,32 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                 }
                 __syncwarp();  // all lanes are done with `buf` before it is refilled
             }
-            // partial[s][req][row]
+            // partial[s][req][row]: the 16 x 16 tile goes through the warp's free
+            // staging buffer (the one just consumed) so each request's 16 rows are
+            // stored as two full 32-byte sectors -- the scattered 4-byte stores
+            // were measured at 8x their bytes in DRAM writes
+            __syncwarp();
+            float* tt = reinterpret_cast<float*>(&stage[warp][buf ^ 1][0][0]);  // [16 req][17]
 #pragma unroll
-            for (int rq = 0; rq < 2; ++rq) {
-                const int req = g + 8 * rq;
+            for (int rq = 0; rq < 2; ++rq)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) tt[(g + 8 * rq) * 17 + q * 8 + 2 * t + e2] = y[rq][q * 2 + e2];
+            __syncwarp();
+            {
+                const int req = lane >> 1, h8 = (lane & 1) * 8;
                 if (req < B) {
+                    float v[8];
 #pragma unroll
-                    for (int q = 0; q < 2; ++q)
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            const int row = rt * kTileRows + q * 8 + 2 * t + e2;
-                            a.partial[s * pstride + (int64_t)req * a.NRT * kTileRows + row] = y[rq][q * 2 + e2];
-                        }
+                    for (int k = 0; k < 8; ++k) v[k] = tt[req * 17 + h8 + k];
+                    float4* dst = reinterpret_cast<float4*>(a.partial + s * pstride + (int64_t)req * a.NRT * kTileRows +
+                                                            rt * kTileRows + h8);
+                    dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                    dst[1] = make_float4(v[4], v[5], v[6], v[7]);
                 }
             }
+            __syncwarp();  // (the buffer is refilled by the next tile's prefetch)
         }
         cp_async_wait<0>();
     }

@@ -532,10 +532,11 @@ __global__ void __launch_bounds__(tcg::kThreads, 2) gemm_tc_kernel(const GemmArg
         auto load_sc = [&](const StepDesc& d) {  // raw scales of a step (converted two steps later)
             Sc c;
             const uint32_t e = d.s + toff;
+            const bool v = tib < (d.f >> 4);  // (rows past the last tile have no scales)
 #pragma unroll
             for (int k = 0; k < kMaxSets; ++k) {
-                c.al[k] = d.i < pk[k] ? __ldg(alp[k] + e) : zero;
-                if constexpr (ASYM) c.z[k] = (d.i == 0 && pk[k] > 0) ? __ldg(zp[k] + e) : zero;
+                c.al[k] = (v && d.i < pk[k]) ? __ldg(alp[k] + e) : zero;
+                if constexpr (ASYM) c.z[k] = (v && d.i == 0 && pk[k] > 0) ? __ldg(zp[k] + e) : zero;
                 else c.z[k] = zero;
             }
             return c;

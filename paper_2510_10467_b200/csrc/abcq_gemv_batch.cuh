@@ -4,16 +4,19 @@
 // lookup, table, TMA helpers) live in abcq_gemv_lut.cuh; DESIGN.md §3.1.
 //
 // One CTA per SM (a co-resident grid) of kWarps warps. The batch's items form
-// one sequence split into cost-balanced CTA ranges (see "Work schedule");
-// a range is processed in rounds of <= 2 (job, slice) pieces, one lookup-table
-// build per round. Every warp is its own producer and consumer: a private
-// kRing-deep ring of shared-memory slots, lane 0 streaming (kK items x one
-// plane) of weights + that plane's scales (+ offsets) per slot with TMA bulk
-// copies (cp.async.bulk ... mbarrier::complete_tx); the warp consumes slot e
-// while slots e+1..e+kRing-1 are in flight, and the slot stream runs on across
-// rounds and jobs (weights are static: it starts before the PDL wait). Jobs
-// split over slices (NS > 1) store 16-row partials; ONE PDL-chained
-// batch_reduce_kernel sums them in a fixed order (bitwise reproducible).
+// one sequence split into cost-balanced CTA ranges (host-computed, see "Work
+// schedule"); a range is processed in rounds of one (job, slice) piece each,
+// the round's lookup table double-buffered and built by a builder group while
+// the previous round streams. Every warp is its own producer and consumer: a
+// private ring of SlotGeom::kRing shared-memory slots, lane 0 streaming
+// (SlotGeom::kK items x one plane) of weights + that plane's scales (+
+// offsets) per slot with TMA bulk copies (cp.async.bulk ...
+// mbarrier::complete_tx); the warp consumes slot e while the later slots are
+// in flight, and the slot stream runs on across rounds and jobs (weights are
+// static: it starts before the PDL wait). Jobs split over slices (NS > 1)
+// store 16-row partials; the split-K sums are completed in a fixed order
+// (bitwise reproducible) by trailing CTAs of this grid (small batches) or by
+// ONE PDL-chained batch_reduce_kernel.
 #pragma once
 #include "abcq_gemv_lut.cuh"
 
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     __syncwarp();
     const int it0 = a.cta_it[b], it1 = a.cta_it[b + 1];
 
-    // ---- this warp's slot stream: rounds -> sub-runs -> chunks of kK items ->
+    // ---- this warp's slot stream: rounds -> sub-runs -> chunks of SlotGeom::kK items ->
     // planes; the issue cursor keeps its source pointers in registers and
     // advances them incrementally (the job table in parameter space is read
     // only when the cursor enters a new sub-run)

@@ -454,3 +454,40 @@ def test_gemm_mixedp_deep_precisions(P, scale_dtype):
             a = a.astype(np.float16).astype(np.float32)
         want = O.gemv_lut(m.bitplanes.words, cols, 128, a, None, p, Xh[b])
         assert O.rel_dev(Y[b], want) <= 1e-4, (b, p, O.rel_dev(Y[b], want))
+
+
+# --- torch.ops.anybcq_b200 (SURVEY §8b device operator) -------------------------
+
+def test_torch_ops_match_device_model(P):
+    from paper_2510_10467_b200 import ops
+    m = synth_model(P, 1024, 4096, 2, 4, seed=11)
+    dm = P.DeviceModel.from_model(m, scale_dtype="f16")
+    h = ops.register(dm)
+    try:
+        x = torch.from_numpy(O.random_gaussian(1, 4096, seed=3).ravel()).cuda().half()
+        for p in (2, 3, 4):
+            y = torch.ops.anybcq_b200.gemv(h, x, p)
+            assert y.dtype == torch.float16 and y.shape == (1024,)
+            assert torch.equal(y, dm.gemv(p, x, out_dtype=torch.float16))   # same launch, bitwise
+        X = torch.randn(3, 4096, device="cuda")
+        Y = torch.ops.anybcq_b200.gemm_mixedp(h, X, [2, 4, 3])
+        assert torch.equal(Y, dm.gemm_mixedp([2, 4, 3], X))
+        W = torch.ops.anybcq_b200.dequantize(h, 3, X)
+        assert torch.equal(W, dm.dequantize(3))
+        torch.library.opcheck(torch.ops.anybcq_b200.gemv.default, (h, x, 3),
+                              test_utils=("test_schema", "test_faketensor"))
+        # the op captures into a CUDA graph (the decode harness path)
+        xs = x.clone()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            torch.ops.anybcq_b200.gemv(h, xs, 3)     # workspace for this stream, outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            yg = torch.ops.anybcq_b200.gemv(h, xs, 3)
+        xs.copy_(x.flip(0))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(yg, dm.gemv(3, x.flip(0).contiguous(), out_dtype=torch.float16))
+    finally:
+        ops.unregister(h)

@@ -57,3 +57,36 @@ def test_product_package_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+# --- torch.ops.anybcq_b200 (SURVEY §8b device operator) -------------------------
+
+class _Shape:  # stands in for a DeviceModel: the fake kernels read only rows/cols
+    rows, cols = 48, 256
+
+
+def test_torch_ops_registered_and_trace_shapes():
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    from paper_2510_10467_b200 import ops
+    for name in ("gemv", "gemm_mixedp", "dequantize"):
+        assert hasattr(torch.ops.anybcq_b200, name)
+    h = ops.register(_Shape())
+    try:
+        with FakeTensorMode():
+            x = torch.empty(256, dtype=torch.float16)
+            assert torch.ops.anybcq_b200.gemv(h, x, 3).shape == (48,)
+            assert torch.ops.anybcq_b200.gemv(h, x, 3).dtype == torch.float16
+            X = torch.empty(3, 256)
+            Y = torch.ops.anybcq_b200.gemm_mixedp(h, X, [2, 4, 3])
+            assert Y.shape == (3, 48) and Y.dtype == torch.float32
+            assert torch.ops.anybcq_b200.dequantize(h, 2, X).shape == (48, 256)
+            with pytest.raises(P.UsageError):
+                torch.ops.anybcq_b200.gemv(h, torch.empty(255), 3)
+            with pytest.raises(P.UsageError):
+                torch.ops.anybcq_b200.gemm_mixedp(h, X, [2, 4])
+    finally:
+        ops.unregister(h)
+    with pytest.raises(P.UsageError):
+        ops.model(h)
+    with pytest.raises(P.UsageError):
+        ops.register(object())

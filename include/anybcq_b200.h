@@ -39,6 +39,11 @@ extern "C" {
 /* element dtypes */
 #define ABCQ_F32 0
 #define ABCQ_F16 1
+/* x dtype of the tiled GEMV only (abcq_gemv / abcq_gemv_batch): x points at
+ * 2*cols f16 values [g ; u] and the GEMV input is x_k = f16(silu(g_k) * u_k),
+ * computed exactly as abcq_silu_mul_f16 (bitwise) while the tables are built --
+ * a decoder's SiLU-gated MLP input without the separate elementwise launch */
+#define ABCQ_F16_SILU_GLU 2
 
 /* plane layouts */
 #define ABCQ_LAYOUT_ROWMAJOR 0 /* reference layout verbatim: (p_hi, rows, ceil(cols/32)) u32 */
@@ -185,6 +190,12 @@ int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype
  *                k, v written to the caches (kv_heads, max_ctx, d) at position pos
  *   attn_decode: one query token over positions [0, ctx) of the caches, GQA,
  *                head_dim 128, heads/kv_heads <= 8; out (heads x 128)
+ *   rope_attn_decode: rope_append + attn_decode over [0, pos] in ONE launch,
+ *                bitwise equal to that pair; q and k are left unrotated (only
+ *                the cache row pos receives the rotated k). The workspace
+ *                (abcq_attn_decode_workspace_bytes(heads, pos + 1)) must be
+ *                zero-filled once before first use: it holds self-resetting
+ *                per-kv-head counters (the last split block combines)
  *   silu_mul:    a = silu(g) * u                                            */
 int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
                          void* stream);
@@ -195,6 +206,10 @@ int abcq_attn_decode_workspace_bytes(int32_t heads, int32_t ctx, size_t* out_byt
 int abcq_attn_decode_f16(const void* d_q, const void* d_kcache, const void* d_vcache, int32_t heads,
                          int32_t kv_heads, int32_t max_ctx, int32_t ctx, float scale, void* d_out, void* d_workspace,
                          size_t workspace_bytes, void* stream);
+int abcq_rope_attn_decode_f16(const void* d_q, const void* d_k, const void* d_v, const float* d_cos,
+                              const float* d_sin, void* d_kcache, void* d_vcache, int32_t heads, int32_t kv_heads,
+                              int32_t max_ctx, int32_t pos, float scale, void* d_out, void* d_workspace,
+                              size_t workspace_bytes, void* stream);
 int abcq_silu_mul_f16(const void* d_g, const void* d_u, void* d_a, int32_t n, void* stream);
 
 #ifdef __cplusplus

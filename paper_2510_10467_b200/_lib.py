@@ -20,6 +20,7 @@ HEADER = PKG.parent / "include" / "anybcq_b200.h"
 
 ABCQ_MAX_PLANES = 16
 F32, F16 = 0, 1
+F16_SILU_GLU = 2  # tiled GEMV x = [g ; u], input f16(silu(g) * u)
 LAYOUT_ROWMAJOR, LAYOUT_TILED = 0, 1
 E_ARG, E_PRECISION, E_LAYOUT, E_WORKSPACE, E_DEVICE = -1, -2, -3, -4, -5
 
@@ -88,6 +89,8 @@ SIGNATURES = {
     "abcq_rope_append_f16": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
     "abcq_attn_decode_workspace_bytes": (C.c_int, [_i32, _i32, C.POINTER(_sz)]),
     "abcq_attn_decode_f16": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp, _sz, _vp]),
+    "abcq_rope_attn_decode_f16": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_float,
+                                            _vp, _vp, _sz, _vp]),
     "abcq_silu_mul_f16": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),
 }
 

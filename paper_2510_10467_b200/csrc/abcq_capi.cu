@@ -49,7 +49,9 @@ int check_call(const abcq_model_t* m, int p, const void* x, int xd, const void* 
     if (!m->alpha[p]) return fail(ABCQ_E_ARG, "scale set %d missing", p);
     if (m->asymmetric && !m->offset[p]) return fail(ABCQ_E_ARG, "offset set %d missing", p);
     if (!x || !y) return fail(ABCQ_E_ARG, "x / y pointer is NULL");
-    if (!dtype_ok(xd) || !dtype_ok(yd)) return fail(ABCQ_E_ARG, "bad x/y dtype");
+    if (!(dtype_ok(xd) || xd == ABCQ_F16_SILU_GLU) || !dtype_ok(yd)) return fail(ABCQ_E_ARG, "bad x/y dtype");
+    if (xd == ABCQ_F16_SILU_GLU && !abcq::lut_supports(m, p))
+        return fail(ABCQ_E_LAYOUT, "the SiLU-gated x dtype needs the tiled layout (group 128)");
     return 0;
 }
 }  // namespace
@@ -193,7 +195,9 @@ static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {
         if (int rc = check_call(J.model, J.p, J.x, J.x_dtype, J.y, J.y_dtype)) return rc;
         if (!abcq::lut_supports(J.model, J.p))
             return fail(ABCQ_E_LAYOUT, "job %d: batched GEMV needs the tiled layout (group 128)", j);
-        if (J.x_dtype != jobs[0].x_dtype || J.y_dtype != jobs[0].y_dtype ||
+        const int xb = J.x_dtype == ABCQ_F16_SILU_GLU ? ABCQ_F16 : J.x_dtype;
+        const int xb0 = jobs[0].x_dtype == ABCQ_F16_SILU_GLU ? ABCQ_F16 : jobs[0].x_dtype;
+        if (xb != xb0 || J.y_dtype != jobs[0].y_dtype ||
             J.model->scale_dtype != m0->scale_dtype || J.model->asymmetric != m0->asymmetric)
             return fail(ABCQ_E_ARG, "job %d: dtypes / mode differ from job 0", j);
     }
@@ -218,13 +222,15 @@ int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t w
     int ps[ABCQ_MAX_PLANES + 16];
     const void* xs[ABCQ_MAX_PLANES + 16];
     void* ys[ABCQ_MAX_PLANES + 16];
+    int xds[ABCQ_MAX_PLANES + 16];
     for (int j = 0; j < n; ++j) {
+        xds[j] = jobs[j].x_dtype;
         models[j] = jobs[j].model;
         ps[j] = jobs[j].p;
         xs[j] = jobs[j].x;
         ys[j] = jobs[j].y;
     }
-    return cuda_ret(abcq::launch_gemv_jobs(models, ps, xs, ys, n, jobs[0].x_dtype, jobs[0].y_dtype, d_ws,
+    return cuda_ret(abcq::launch_gemv_jobs(models, ps, xs, ys, n, xds, jobs[0].y_dtype, d_ws,
                                            (cudaStream_t)stream),
                     "abcq_gemv_batch");
 }
@@ -264,6 +270,7 @@ int abcq_gemm_mixedp(const abcq_model_t* m, int32_t B, const int32_t* p_host, co
 
 int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
                     int32_t y_dtype, void* stream) {
+    if (x_dtype == ABCQ_F16_SILU_GLU) return fail(ABCQ_E_ARG, "abcq_gemv_naive: x must be f16 or f32");
     if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;
     return cuda_ret(abcq::launch_gemv_generic(m, p, d_x, x_dtype, d_y, y_dtype, 1, (cudaStream_t)stream),
                     "abcq_gemv_naive");
@@ -314,6 +321,20 @@ int abcq_attn_decode_f16(const void* d_q, const void* d_kcache, const void* d_vc
     return cuda_ret(abcq::launch_attn_decode(d_q, d_kcache, d_vcache, heads, kv_heads, max_ctx, ctx, scale, d_out,
                                              d_workspace, (cudaStream_t)stream),
                     "abcq_attn_decode_f16");
+}
+
+int abcq_rope_attn_decode_f16(const void* d_q, const void* d_k, const void* d_v, const float* d_cos,
+                              const float* d_sin, void* d_kcache, void* d_vcache, int32_t heads, int32_t kv_heads,
+                              int32_t max_ctx, int32_t pos, float scale, void* d_out, void* d_workspace,
+                              size_t workspace_bytes, void* stream) {
+    if (!d_q || !d_k || !d_v || !d_cos || !d_sin || !d_kcache || !d_vcache || !d_out || kv_heads < 1 ||
+        heads % kv_heads || heads / kv_heads > 8 || pos < 0 || pos >= max_ctx)
+        return fail(ABCQ_E_ARG, "abcq_rope_attn_decode_f16: bad arguments (head_dim must be 128, heads/kv_heads <= 8)");
+    if (!d_workspace || workspace_bytes < abcq::attn_decode_workspace_bytes(heads, pos + 1))
+        return fail(ABCQ_E_WORKSPACE, "abcq_rope_attn_decode_f16: workspace too small");
+    return cuda_ret(abcq::launch_rope_attn_decode(d_q, d_k, d_v, d_cos, d_sin, d_kcache, d_vcache, heads, kv_heads,
+                                                  max_ctx, pos, scale, d_out, d_workspace, (cudaStream_t)stream),
+                    "abcq_rope_attn_decode_f16");
 }
 
 int abcq_silu_mul_f16(const void* d_g, const void* d_u, void* d_a, int32_t n, void* stream) {

@@ -116,62 +116,204 @@ __global__ void rope_append_kernel(__half* __restrict__ q, __half* __restrict__ 
 // grid (kv_heads, splits); block = 32 * g threads: warp w owns query head
 // kh*g + w; lane l owns positions l, l+32 of the split (scores) and dims
 // 4l..4l+3 (output). Partials: m, l and acc[128] per (head, split).
-constexpr int kAttnSplit = 64;
+constexpr int kAttnSplit = 64;  // positions per block
 constexpr int kPartStride = 4 + 128;  // m, l, pad, pad, acc[128] (16-byte aligned acc)
+// stage rows [p0, p0 + n) of one kv head's K and V (d = 128) in shared memory,
+// zero-filling rows >= n and skipping row `skip`: 16-byte loads, all of a
+// thread's loads issued before its stores (a split is 32 KB; 4-byte copies
+// left the loads latency-bound at ~0.4 TB/s)
+template <int NR>
+__device__ __forceinline__ void stage_kv(const __half* __restrict__ kc, const __half* __restrict__ vc, int kh,
+                                         int lmax, int p0, int n, int skip, __half (*ks)[128 + 2],
+                                         __half (*vs)[128]) {
+    constexpr int d = 128, kVec = NR * d / 8;
+    for (int base = 0; base < kVec; base += 8 * (int)blockDim.x) {
+        uint4 kr[8], vr[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = base + threadIdx.x + j * blockDim.x, r = i >> 4, c8 = (i & 15) * 8;
+            kr[j] = vr[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (i < kVec && r < n && r != skip) {
+                kr[j] = __ldg(reinterpret_cast<const uint4*>(kc + ((size_t)kh * lmax + p0 + r) * d + c8));
+                vr[j] = __ldg(reinterpret_cast<const uint4*>(vc + ((size_t)kh * lmax + p0 + r) * d + c8));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int i = base + threadIdx.x + j * blockDim.x, r = i >> 4, c8 = (i & 15) * 8;
+            if (i < kVec && r != skip) {  // (row `skip` is the caller's)
+                uint32_t* kd = reinterpret_cast<uint32_t*>(&ks[r][c8]);  // odd-word row stride: 4-byte stores
+                kd[0] = kr[j].x;
+                kd[1] = kr[j].y;
+                kd[2] = kr[j].z;
+                kd[3] = kr[j].w;
+                *reinterpret_cast<uint4*>(&vs[r][c8]) = vr[j];
+            }
+        }
+    }
+}
+
+// one warp = one query head over the staged split: scores (lane = row), the
+// split's max / sum of exponentials, and the exp-weighted V rows (lane = dims
+// 4l..4l+3) -> part = {m, l, -, -, acc[128]}. Independent partial chains
+// (4 per dot product, 2 over the V rows) keep the FMA latency off the
+// critical path.
+__device__ __forceinline__ void split_attend(const __half* qh, const __half (*ks)[128 + 2],
+                                             const __half (*vs)[128], int n, float scale, int lane, float* pp) {
+    constexpr int d = 128, RPL = kAttnSplit / 32;
+    float s[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        const int r = lane + 32 * j;
+        float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int c = 0; c < d; c += 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 qq = __half22float2(*reinterpret_cast<const __half2*>(qh + c + 2 * u));
+                const float2 kk = __half22float2(*reinterpret_cast<const __half2*>(&ks[r][c + 2 * u]));
+                a4[u] = fmaf(qq.x, kk.x, fmaf(qq.y, kk.y, a4[u]));
+            }
+        }
+        s[j] = r < n ? ((a4[0] + a4[1]) + (a4[2] + a4[3])) * scale : -INFINITY;
+    }
+    float mx = s[0];
+#pragma unroll
+    for (int j = 1; j < RPL; ++j) mx = fmaxf(mx, s[j]);
+    const float m = warp_max(mx);
+    float e[RPL], es = 0.f;
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        e[j] = __expf(s[j] - m);
+        es += e[j];
+    }
+    const float l = warp_sum(es);
+    float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
+    auto pick = [&](int r) {
+        float ej = e[0];
+#pragma unroll
+        for (int j = 1; j < RPL; ++j) ej = (r >> 5) == j ? e[j] : ej;
+        return __shfl_sync(0xffffffffu, ej, r & 31);
+    };
+    auto row = [&](int r, float pr, float (&oo)[4]) {
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&vs[r][4 * lane]));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&vs[r][4 * lane + 2]));
+        oo[0] = fmaf(pr, a.x, oo[0]);
+        oo[1] = fmaf(pr, a.y, oo[1]);
+        oo[2] = fmaf(pr, b.x, oo[2]);
+        oo[3] = fmaf(pr, b.y, oo[3]);
+    };
+    int r = 0;
+#pragma unroll 4
+    for (; r + 1 < n; r += 2) {  // rows r, r+1 into two independent chains
+        const float p0 = pick(r), p1 = pick(r + 1);
+        row(r, p0, o0);
+        row(r + 1, p1, o1);
+    }
+    if (r < n) row(r, pick(r), o0);
+    if (lane == 0) {
+        pp[0] = m;
+        pp[1] = l;
+    }
+    *reinterpret_cast<float4*>(pp + 4 + 4 * lane) =
+        make_float4(o0[0] + o1[0], o0[1] + o1[1], o0[2] + o1[2], o0[3] + o1[3]);
+}
+
 __global__ void attn_decode_partial(const __half* __restrict__ q, const __half* __restrict__ kc,
                                     const __half* __restrict__ vc, int heads, int kv_heads, int lmax, int L,
                                     float scale, float* __restrict__ part) {
     pdl_enter();
     constexpr int d = 128;
     __shared__ __half ks[kAttnSplit][d + 2];  // odd word stride: lane-per-row dots are conflict-free
-    __shared__ __half vs[kAttnSplit][d];
+    __shared__ __align__(16) __half vs[kAttnSplit][d];
     const int kh = blockIdx.x, sp = blockIdx.y, g = heads / kv_heads;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p0 = sp * kAttnSplit, n = min(kAttnSplit, L - p0);
-    for (int i = threadIdx.x; i < kAttnSplit * d / 2; i += blockDim.x) {  // 4-byte copies
-        const int r = i / (d / 2), c2 = (i % (d / 2)) * 2;
-        __half2 kv = __floats2half2_rn(0.f, 0.f), vv = kv;
-        if (r < n) {
-            kv = *reinterpret_cast<const __half2*>(kc + ((size_t)kh * lmax + p0 + r) * d + c2);
-            vv = *reinterpret_cast<const __half2*>(vc + ((size_t)kh * lmax + p0 + r) * d + c2);
-        }
-        *reinterpret_cast<__half2*>(&ks[r][c2]) = kv;
-        *reinterpret_cast<__half2*>(&vs[r][c2]) = vv;
-    }
+    stage_kv<kAttnSplit>(kc, vc, kh, lmax, p0, n, -1, ks, vs);
     __syncthreads();
     const int h = kh * g + warp;
-    const __half* qh = q + (size_t)h * d;
-    float s[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int r = lane + 32 * j;
-        float acc = 0.f;
-        for (int c = 0; c < d; c += 2) {
-            const float2 qq = __half22float2(*reinterpret_cast<const __half2*>(qh + c));
-            const float2 kk = __half22float2(*reinterpret_cast<const __half2*>(&ks[r][c]));
-            acc = fmaf(qq.x, kk.x, fmaf(qq.y, kk.y, acc));
+    split_attend(q + (size_t)h * d, ks, vs, n, scale, lane, part + ((size_t)h * gridDim.y + sp) * kPartStride);
+}
+
+// RoPE + KV append + split-L partials + combine in ONE launch (the decode
+// step's attention; replaces rope_append_kernel -> attn_decode_partial ->
+// attn_decode_combine, bitwise equal to that sequence). grid (kv_heads,
+// splits) over positions [0, pos]; block = 32 * g threads. Each warp rotates
+// its own query head into shared memory (q itself is left untouched); the
+// block whose split holds `pos` rotates the new key, writes k and v to the
+// caches and uses them from shared memory (no other split reads `pos`). The
+// last block of a kv head to finish (a per-head counter, zero-filled once,
+// self-resetting) combines that head group's partials.
+__global__ void rope_attn_decode_fused(const __half* __restrict__ q, const __half* __restrict__ k,
+                                       const __half* __restrict__ v, const float* __restrict__ cosv,
+                                       const float* __restrict__ sinv, __half* __restrict__ kc,
+                                       __half* __restrict__ vc, int heads, int kv_heads, int lmax, int pos,
+                                       float scale, float* __restrict__ part, unsigned* __restrict__ cnt,
+                                       __half* __restrict__ out) {
+    pdl_enter();
+    constexpr int d = 128, h2 = d / 2;
+    __shared__ __half ks[kAttnSplit][d + 2];
+    __shared__ __align__(16) __half vs[kAttnSplit][d];
+    __shared__ __align__(16) __half qs[8][d];
+    __shared__ int last;
+    const int kh = blockIdx.x, sp = blockIdx.y, g = heads / kv_heads, splits = gridDim.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = pos + 1, p0 = sp * kAttnSplit, n = min(kAttnSplit, L - p0);
+    const int h = kh * g + warp;
+    for (int t = lane; t < h2; t += 32) {  // rope_append_kernel's expression, per query head
+        const float x1 = __half2float(q[(size_t)h * d + t]), x2 = __half2float(q[(size_t)h * d + t + h2]);
+        const float c = cosv[t], s = sinv[t];
+        qs[warp][t] = __float2half_rn(x1 * c - x2 * s);
+        qs[warp][t + h2] = __float2half_rn(x2 * c + x1 * s);
+    }
+    const int rnew = pos - p0;  // the new token's row, if it lies in this split
+    stage_kv<kAttnSplit>(kc, vc, kh, lmax, p0, n, rnew, ks, vs);
+    if (rnew >= 0 && rnew < n) {
+        for (int t = threadIdx.x; t < h2; t += blockDim.x) {
+            const float x1 = __half2float(k[(size_t)kh * d + t]), x2 = __half2float(k[(size_t)kh * d + t + h2]);
+            const float c = cosv[t], s = sinv[t];
+            const __half o1 = __float2half_rn(x1 * c - x2 * s), o2 = __float2half_rn(x2 * c + x1 * s);
+            const __half v1 = v[(size_t)kh * d + t], v2 = v[(size_t)kh * d + t + h2];
+            ks[rnew][t] = o1;
+            ks[rnew][t + h2] = o2;
+            vs[rnew][t] = v1;
+            vs[rnew][t + h2] = v2;
+            __half* kdst = kc + ((size_t)kh * lmax + pos) * d;
+            __half* vdst = vc + ((size_t)kh * lmax + pos) * d;
+            kdst[t] = o1;
+            kdst[t + h2] = o2;
+            vdst[t] = v1;
+            vdst[t + h2] = v2;
         }
-        s[j] = r < n ? acc * scale : -INFINITY;
     }
-    const float m = warp_max(fmaxf(s[0], s[1]));
-    const float e0 = __expf(s[0] - m), e1 = __expf(s[1] - m);
-    const float l = warp_sum(e0 + e1);
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int r = 0; r < n; ++r) {
-        const float pr = __shfl_sync(0xffffffffu, r < 32 ? e0 : e1, r & 31);
-        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&vs[r][4 * lane]));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&vs[r][4 * lane + 2]));
-        o[0] = fmaf(pr, a.x, o[0]);
-        o[1] = fmaf(pr, a.y, o[1]);
-        o[2] = fmaf(pr, b.x, o[2]);
-        o[3] = fmaf(pr, b.y, o[3]);
+    __syncthreads();
+    split_attend(qs[warp], ks, vs, n, scale, lane, part + ((size_t)h * splits + sp) * kPartStride);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&cnt[kh * 32], 1u);
+        last = prev == (unsigned)splits - 1;
+        if (last) cnt[kh * 32] = 0;  // self-reset for the next launch
     }
-    float* pp = part + ((size_t)h * gridDim.y + sp) * kPartStride;
-    if (lane == 0) {
-        pp[0] = m;
-        pp[1] = l;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // attn_decode_combine's arithmetic for the g heads of this kv head: warp w, dims 4l..4l+3
+    const float* ph = part + (size_t)h * splits * kPartStride;
+    float M = -INFINITY;
+    for (int t = 0; t < splits; ++t) M = fmaxf(M, __ldcg(ph + t * kPartStride));
+    float num[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
+    for (int t = 0; t < splits; ++t) {
+        const float w = __expf(__ldcg(ph + t * kPartStride) - M);
+        den = fmaf(w, __ldcg(ph + t * kPartStride + 1), den);
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(ph + t * kPartStride + 4 + 4 * lane));
+        num[0] = fmaf(w, a.x, num[0]);
+        num[1] = fmaf(w, a.y, num[1]);
+        num[2] = fmaf(w, a.z, num[2]);
+        num[3] = fmaf(w, a.w, num[3]);
     }
-    *reinterpret_cast<float4*>(pp + 4 + 4 * lane) = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[(size_t)h * d + 4 * lane + j] = __float2half_rn(num[j] / den);
 }
 
 // one block of 128 threads per head: out[h] = sum_s e^{m_s - M} acc_s / sum_s e^{m_s - M} l_s
@@ -214,8 +356,25 @@ int launch_rope_append(void* q, void* k, const void* v, const float* cosv, const
                            static_cast<__half*>(kc), static_cast<__half*>(vc), heads, kv_heads, d, lmax, pos);
 }
 
-size_t attn_decode_workspace_bytes(int heads, int L) {
+// partials, then one counter per kv head on its own 128-byte line (fused kernel)
+size_t attn_decode_part_bytes(int heads, int L) {
     return (size_t)heads * ((L + kAttnSplit - 1) / kAttnSplit) * kPartStride * sizeof(float);
+}
+size_t attn_decode_workspace_bytes(int heads, int L) {
+    return attn_decode_part_bytes(heads, L) + (size_t)heads * 32 * sizeof(unsigned);
+}
+
+int launch_rope_attn_decode(const void* q, const void* k, const void* v, const float* cosv, const float* sinv,
+                            void* kc, void* vc, int heads, int kv_heads, int lmax, int pos, float scale, void* out,
+                            void* ws, cudaStream_t st) {
+    const int splits = (pos + 1 + kAttnSplit - 1) / kAttnSplit;
+    float* part = static_cast<float*>(ws);
+    unsigned* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + attn_decode_part_bytes(heads, pos + 1));
+    return (int)launch_pdl(rope_attn_decode_fused, dim3(kv_heads, splits), dim3(32 * (heads / kv_heads)), st,
+                           static_cast<const __half*>(q), static_cast<const __half*>(k),
+                           static_cast<const __half*>(v), cosv, sinv, static_cast<__half*>(kc),
+                           static_cast<__half*>(vc), heads, kv_heads, lmax, pos, scale, part, cnt,
+                           static_cast<__half*>(out));
 }
 
 int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads, int kv_heads, int lmax, int L,

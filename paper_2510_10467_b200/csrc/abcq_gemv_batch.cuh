@@ -35,6 +35,7 @@ struct Job {
     void* y;
     float* partial;      // [NRT][NS][16]: a row tile's slice partials are one contiguous run
     int rows, cols, NRT, NS, p, items;
+    int glu;        // x = [g ; u] (2*cols f16): input f16(silu(g) * u) (ABCQ_F16_SILU_GLU)
     uint32_t* arrive;   // CTAs done streaming this job (split jobs; self-resetting)
     uint32_t* reduced;  // reduce blocks done with this job (self-resetting)
     int ncta;           // CTAs whose range touches this job
@@ -445,13 +446,14 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     bool has1 = false;
     const XT* xp0 = nullptr;
     const XT* xp1 = nullptr;
-    int xk0 = 0, xk1 = 0, xc0 = 0, xc1 = 0;
+    int xk0 = 0, xk1 = 0, xc0 = 0, xc1 = 0, xg0 = 0, xg1 = 0;
     if (has0) {
         R0 = make_round(a, it0, it1);
         const Job& J0 = a.jobs[R0.pc[0].j];
         xp0 = static_cast<const XT*>(J0.x);
         xk0 = R0.pc[0].s * kSliceCols + 8 * (tid & 31);
         xc0 = J0.cols;
+        xg0 = J0.glu;
         has1 = R0.end < it1;
         if (has1) {
             R1 = make_round(a, R0.end, it1);
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             xp1 = static_cast<const XT*>(J1.x);
             xk1 = R1.pc[0].s * kSliceCols + 8 * (tid & 31);
             xc1 = J1.cols;
+            xg1 = J1.glu;
         }
     }
     const int half = lane >> 4, r = lane & 15;
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     };
     auto piece_x = [&](const Round& Rn, int c, float (&xv)[8]) {
         const Job& Jn = a.jobs[Rn.pc[0].j];
-        load_x8<XT>(static_cast<const XT*>(Jn.x), Rn.pc[0].s * kSliceCols + 8 * c, Jn.cols, xv);
+        load_x8_any<XT>(static_cast<const XT*>(Jn.x), Rn.pc[0].s * kSliceCols + 8 * c, Jn.cols, Jn.glu, xv);
     };
 
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
@@ -506,8 +509,8 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
     {
         float xv0[8], xv1[8];
-        if (has0) load_x8<XT>(xp0, xk0, xc0, xv0);
-        if (has1) load_x8<XT>(xp1, xk1, xc1, xv1);
+        if (has0) load_x8_any<XT>(xp0, xk0, xc0, xg0, xv0);
+        if (has1) load_x8_any<XT>(xp1, xk1, xc1, xg1, xv1);
         for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
             issue(ic, s_fill);
             advance(ic);

@@ -58,6 +58,7 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.alpha = m->alpha[p];
     J.offset = m->asymmetric ? m->offset[p] : nullptr;
     J.x = x;
+    J.glu = 0;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
     J.ncta = 0;
@@ -70,7 +71,7 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 }
 
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st) {
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st) {
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
     // fixed cost of a (job, slice) piece in blocks: measured best 300 for
@@ -85,6 +86,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     uint32_t* counters = part_total ? reinterpret_cast<uint32_t*>(w + part_total) : nullptr;
     for (int j = 0; j < n; ++j) {
         make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
+        a.jobs[j].glu = x_dtypes[j] == ABCQ_F16_SILU_GLU;
         w += partial_bytes(models[j]);
         a.jobs[j].arrive = counters ? counters + j * kCounterStride : nullptr;
         a.jobs[j].reduced = counters ? counters + (kMaxJobs + j) * kCounterStride : nullptr;
@@ -198,13 +200,13 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
     const abcq_model_t* m = models[0];
     const bool asym = m->asymmetric != 0;
-    return x_dtype == ABCQ_F16 ? launch_yt<__half>(a, y_dtype, m->scale_dtype, asym, grid, st)
+    return x_dtypes[0] != ABCQ_F32 ? launch_yt<__half>(a, y_dtype, m->scale_dtype, asym, grid, st)
                                : launch_yt<float>(a, y_dtype, m->scale_dtype, asym, grid, st);
 }
 
 int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
                     void* ws, cudaStream_t st) {
-    return launch_gemv_jobs(&m, &p, &x, &y, 1, x_dtype, y_dtype, ws, st);
+    return launch_gemv_jobs(&m, &p, &x, &y, 1, &x_dtype, y_dtype, ws, st);
 }
 
 }  // namespace abcq

@@ -110,6 +110,40 @@ __device__ __forceinline__ void load_x8(const XT* x, int k0, int cols, float (&x
     }
 }
 
+// x = [g ; u] (2*cols f16, ABCQ_F16_SILU_GLU): the input is f16(silu(g) * u),
+// the same expression as silu_mul_kernel (abcq_decode_ops.cu) -> bitwise equal
+__device__ __forceinline__ float silu_glu(__half g, __half u) {
+    const float gv = __half2float(g);
+    return __half2float(__float2half_rn(gv / (1.f + __expf(-gv)) * __half2float(u)));
+}
+
+template <typename XT>
+__device__ __forceinline__ void load_x8_glu(const XT* x, int k0, int cols, float (&xs)[8]) {
+    if constexpr (sizeof(XT) == 2) {
+        const __half* g = reinterpret_cast<const __half*>(x);
+        const __half* u = g + cols;
+        if (k0 + 8 <= cols && (cols & 7) == 0) {
+            const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g + k0));
+            const uint4 uv = __ldg(reinterpret_cast<const uint4*>(u + k0));
+            const __half* gh = reinterpret_cast<const __half*>(&gv);
+            const __half* uh = reinterpret_cast<const __half*>(&uv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xs[j] = silu_glu(gh[j], uh[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xs[j] = (k0 + j < cols) ? silu_glu(g[k0 + j], u[k0 + j]) : 0.f;
+        }
+    } else {
+        load_x8<XT>(x, k0, cols, xs);  // (f32 x has no gated form; the host rejects it)
+    }
+}
+
+template <typename XT>
+__device__ __forceinline__ void load_x8_any(const XT* x, int k0, int cols, int glu, float (&xs)[8]) {
+    if (glu) load_x8_glu<XT>(x, k0, cols, xs);
+    else load_x8<XT>(x, k0, cols, xs);
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

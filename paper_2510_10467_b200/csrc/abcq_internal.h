@@ -24,7 +24,7 @@ int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, vo
 // batch of n independent GEMVs (same dtypes / mode), workspaces concatenated
 // in job order (lut_workspace_bytes each)
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, int x_dtype, int y_dtype, void* ws, cudaStream_t st);
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st);
 int lut_max_jobs();
 
 // small-batch mixed-precision GEMM (tensor cores), B <= 16
@@ -44,6 +44,9 @@ int launch_add_rmsnorm(void* x, const void* r, const void* w, void* y, int n, fl
 int launch_rope_append(void* q, void* k, const void* v, const float* cosv, const float* sinv, void* kc, void* vc,
                        int heads, int kv_heads, int d, int lmax, int pos, cudaStream_t st);
 size_t attn_decode_workspace_bytes(int heads, int L);
+int launch_rope_attn_decode(const void* q, const void* k, const void* v, const float* cosv, const float* sinv,
+                            void* kc, void* vc, int heads, int kv_heads, int lmax, int pos, float scale, void* out,
+                            void* ws, cudaStream_t st);
 int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads, int kv_heads, int lmax, int L,
                        float scale, void* out, void* ws, cudaStream_t st);
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st);

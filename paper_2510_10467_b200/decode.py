@@ -17,9 +17,12 @@ the whole step is captured in one CUDA graph).
 
 Per layer the quantized step issues 4 GEMV launches (abcq_gemv_batch):
 [q, k, v] (same x), [o], [gate, up] (same x), [down], plus the fused
-harness ops of abcq_decode_ops.cu (add+RMSNorm x2, RoPE+KV append, split-L
-decode attention, SiLU*up) -- the fp16 comparator uses the same fused ops,
-so the two differ only in the linears.
+harness ops of abcq_decode_ops.cu (add+RMSNorm x2, and RoPE + KV append +
+split-L decode attention + combine as ONE launch) -- the fp16 comparator uses
+the same fused ops. SiLU(gate)*up
+is formed inside the down GEMV's table build (x dtype ABCQ_F16_SILU_GLU over the
+[gate ; up] buffer, bitwise equal to the separate silu_mul launch, which the
+fp16 comparator and `fuse_glu=False` still issue).
 """
 
 from __future__ import annotations
@@ -93,12 +96,19 @@ class _Attention:
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         n = C.c_size_t()
         _lib.check(_lib.lib().abcq_attn_decode_workspace_bytes(cfg.heads, self.lmax, C.byref(n)))
-        self.ws = torch.empty(int(n.value), dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(int(n.value), dtype=torch.uint8, device=device)  # (fused: self-resetting counters)
+        self.fused = True  # rope + append + attention + combine in one launch
         self.out = torch.empty(cfg.hidden, dtype=torch.float16, device=device)
 
     def __call__(self, layer: int, q, k, v):
         cfg, L = self.cfg, _lib.lib()
         kc, vc = self.k_cache[layer], self.v_cache[layer]
+        if self.fused:
+            _lib.check(L.abcq_rope_attn_decode_f16(
+                q.data_ptr(), k.data_ptr(), v.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(), kc.data_ptr(),
+                vc.data_ptr(), cfg.heads, cfg.kv_heads, self.lmax, self.ctx, self.scale, self.out.data_ptr(),
+                self.ws.data_ptr(), self.ws.numel(), _stream()), "abcq_rope_attn_decode_f16")
+            return self.out
         _lib.check(L.abcq_rope_append_f16(q.data_ptr(), k.data_ptr(), v.data_ptr(), self.cos.data_ptr(),
                                           self.sin.data_ptr(), kc.data_ptr(), vc.data_ptr(), cfg.heads,
                                           cfg.kv_heads, cfg.head_dim, self.lmax, self.ctx, _stream()),
@@ -113,8 +123,8 @@ class QuantizedLlamaStep:
     """Decode step with AnyBCQ linears at precision p (p_lo..p_hi resident)."""
 
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), p: int = 3, p_lo: int = 2, p_hi: int = 4,
-                 ctx: int = 1024, device=None, seed: int = 0):
-        self.cfg, self.p = cfg, p
+                 ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True):
+        self.cfg, self.p, self.fuse_glu = cfg, p, fuse_glu
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.layers = []
@@ -140,7 +150,8 @@ class QuantizedLlamaStep:
         self.x = torch.randn(hd, **f16, generator=gen)
         self.q, self.k, self.v = torch.empty(hd, **f16), torch.empty(kvd, **f16), torch.empty(kvd, **f16)
         self.o = torch.empty(hd, **f16)
-        self.g, self.u = torch.empty(inter, **f16), torch.empty(inter, **f16)
+        self.gu = torch.empty(2 * inter, **f16)   # [gate ; up]: the down GEMV's SiLU-gated input
+        self.g, self.u = self.gu[:inter], self.gu[inter:]
         self.d = torch.empty(hd, **f16)
         self.h, self.act = torch.empty(hd, **f16), torch.empty(inter, **f16)
         self.token = torch.empty((), device=self.device, dtype=torch.int64)
@@ -161,8 +172,11 @@ class QuantizedLlamaStep:
             mats["o"].gemv(p, a, out=self.o)
             add_rmsnorm(self.x, self.o, self.norm_w[li][1], self.h, cfg.eps)
             gemv_batch([(mats["gate"], p, self.h, self.g), (mats["up"], p, self.h, self.u)])
-            silu_mul(self.g, self.u, self.act)
-            mats["down"].gemv(p, self.act, out=self.d)
+            if self.fuse_glu:  # silu(gate)*up formed inside the down GEMV's table build
+                mats["down"].gemv(p, self.gu, out=self.d, silu_glu=True)
+            else:
+                silu_mul(self.g, self.u, self.act)
+                mats["down"].gemv(p, self.act, out=self.d)
             resid = self.d
         add_rmsnorm(self.x, resid, self.final_norm, self.h, cfg.eps)
         torch.argmax(torch.mv(self.lm_head, self.h), out=self.token)

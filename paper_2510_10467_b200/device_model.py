@@ -237,10 +237,20 @@ class DeviceModel:
         return x.contiguous()
 
     def gemv(self, p: int, x: torch.Tensor, out: torch.Tensor | None = None,
-             out_dtype: torch.dtype = torch.float32, stream=None) -> torch.Tensor:
-        """y = W_p x on the device, asynchronous on `stream` (default: current)."""
+             out_dtype: torch.dtype = torch.float32, stream=None, silu_glu: bool = False) -> torch.Tensor:
+        """y = W_p x on the device, asynchronous on `stream` (default: current).
+
+        silu_glu: x is [g ; u] (2*cols f16) and the input is f16(silu(g)*u),
+        formed while the tables are built (ABCQ_F16_SILU_GLU; tiled layout)."""
         self._check_p(p)
-        x = self._check_x(x)
+        if silu_glu:
+            if not isinstance(x, torch.Tensor) or x.device != self.device or x.dtype != torch.float16:
+                raise UsageError(f"silu_glu x must be a float16 tensor on {self.device}")
+            if x.numel() != 2 * self.cols:
+                raise UsageError(f"silu_glu input length {x.numel()} != 2*cols {2 * self.cols}")
+            x = x.contiguous()
+        else:
+            x = self._check_x(x)
         self._order_after_upload(p, stream)
         if out is None:
             out = torch.empty(self.rows, dtype=out_dtype, device=self.device)
@@ -248,8 +258,8 @@ class DeviceModel:
             raise UsageError("out must be a contiguous tensor of `rows` elements")
         ws = self.workspace(stream)
         _lib.check(_lib.lib().abcq_gemv(
-            self.struct_ptr(), p, x.data_ptr(), dtype_code(x.dtype), out.data_ptr(),
-            dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv")
+            self.struct_ptr(), p, x.data_ptr(), _lib.F16_SILU_GLU if silu_glu else dtype_code(x.dtype),
+            out.data_ptr(), dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv")
         return out
 
     def gemm_mixedp(self, ps, X: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:

@@ -49,3 +49,17 @@ def test_argument_errors_without_device():
     with pytest.raises(Exception):
         _lib.check(_lib.E_PRECISION)
     assert lib.abcq_lut_build(0x10, 0, 8, 9, 0x20, None) == _lib.E_ARG
+
+
+def test_silu_glu_dtype_validation_without_device():
+    lib = _lib.lib()
+    m = _lib.AbcqModel()
+    m.rows, m.cols, m.group_size, m.p_lo, m.p_hi = 16, 256, 64, 2, 4
+    m.layout, m.scale_dtype, m.planes = _lib.LAYOUT_ROWMAJOR, _lib.F32, 0x1000
+    m.alpha[2] = 0x4000
+    # the gated input exists only for the tiled kernel, and never for the naive path
+    assert lib.abcq_gemv(C.byref(m), 2, 0x2000, _lib.F16_SILU_GLU, 0x3000, 0, None, 0, None) == _lib.E_LAYOUT
+    assert "SiLU-gated" in _lib.last_error()
+    assert lib.abcq_gemv_naive(C.byref(m), 2, 0x2000, _lib.F16_SILU_GLU, 0x3000, 0, None) == _lib.E_ARG
+    assert lib.abcq_gemv(C.byref(m), 2, 0x2000, 3, 0x3000, 0, None, 0, None) == _lib.E_ARG
+    assert lib.abcq_gemv(C.byref(m), 2, 0x2000, 0, 0x3000, _lib.F16_SILU_GLU, None, 0, None) == _lib.E_ARG

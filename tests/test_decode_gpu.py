@@ -33,6 +33,7 @@ def test_rope_append_and_attention_decode():
     g = torch.Generator(device="cuda").manual_seed(1)
     ctx = 300
     att = _Attention(cfg, ctx, torch.device("cuda"), g)
+    att.fused = False   # the separate launches (rotate q/k in place); the fused kernel is checked against them
     q = torch.randn(cfg.hidden, device="cuda", generator=g).half()
     k = torch.randn(1024, device="cuda", generator=g).half()
     v = torch.randn(1024, device="cuda", generator=g).half()
@@ -66,3 +67,46 @@ def test_quantized_step_runs_and_is_deterministic():
     t2 = m.step().item()
     assert t1 == t2 and 0 <= t1 < 1000
     assert time_step(m, iters=2, warmup=1) > 0
+
+
+def test_quantized_step_fused_glu_equals_separate_silu_mul():
+    from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    cfg = LlamaConfig(layers=2, vocab=1000)
+    m = QuantizedLlamaStep(cfg, p=3, ctx=64, fuse_glu=True)
+    x0 = m.x.clone()
+    k0, v0 = m.attn.k_cache.clone(), m.attn.v_cache.clone()
+    t1 = m.step().item()
+    x1, d1 = m.x.clone(), m.d.clone()
+    m.x.copy_(x0)
+    m.attn.k_cache.copy_(k0)
+    m.attn.v_cache.copy_(v0)
+    m.fuse_glu = False
+    t2 = m.step().item()
+    assert t1 == t2
+    assert torch.equal(m.d, d1) and torch.equal(m.x, x1)   # bitwise: same f16 input to the down GEMV
+
+
+@pytest.mark.parametrize("ctx", [1024, 63, 64, 300, 0])
+def test_fused_rope_attention_equals_separate_launches(ctx):
+    """rope_append + attn_decode (+ combine) vs the one-launch fused kernel: bitwise,
+    including the new cache row; repeated launches exercise the counter self-reset."""
+    from paper_2510_10467_b200.decode import LlamaConfig, _Attention
+    cfg = LlamaConfig(layers=2)
+    g = torch.Generator(device="cuda").manual_seed(ctx + 7)
+    att = _Attention(cfg, ctx, torch.device("cuda"), g)
+    q = torch.randn(cfg.hidden, device="cuda", generator=g).half()
+    k = torch.randn(1024, device="cuda", generator=g).half()
+    v = torch.randn(1024, device="cuda", generator=g).half()
+    kc0, vc0 = att.k_cache.clone(), att.v_cache.clone()
+    att.fused = False
+    want = att(1, q.clone(), k.clone(), v.clone()).clone()
+    kc1, vc1 = att.k_cache.clone(), att.v_cache.clone()
+    att.fused = True
+    for _ in range(3):
+        att.k_cache.copy_(kc0)
+        att.v_cache.copy_(vc0)
+        qq, kk = q.clone(), k.clone()
+        got = att(1, qq, kk, v).clone()
+        assert torch.equal(got, want)
+        assert torch.equal(att.k_cache, kc1) and torch.equal(att.v_cache, vc1)
+        assert torch.equal(qq, q) and torch.equal(kk, k)   # inputs left unrotated

@@ -491,3 +491,31 @@ def test_torch_ops_match_device_model(P):
         assert torch.equal(yg, dm.gemv(3, x.flip(0).contiguous(), out_dtype=torch.float16))
     finally:
         ops.unregister(h)
+
+
+# --- SiLU-gated input (ABCQ_F16_SILU_GLU): silu(g)*u formed in the table build ----
+
+@pytest.mark.parametrize("rows,cols,asym", [(4096, 14336, False), (256, 1024, True), (37, 200, False),
+                                            (48, 1000, True)])
+def test_silu_glu_input_matches_separate_silu_mul(P, rows, cols, asym):
+    from paper_2510_10467_b200.decode import silu_mul
+    m = synth_model(P, rows, cols, 2, 4, asym=asym, seed=rows ^ cols)
+    dm = P.DeviceModel.from_model(m, scale_dtype="f16")
+    g = torch.Generator(device="cuda").manual_seed(cols)
+    gu = (2 * torch.randn(2 * cols, device="cuda", generator=g)).half()
+    act = torch.empty(cols, device="cuda", dtype=torch.float16)
+    silu_mul(gu[:cols], gu[cols:], act)
+    for p in (2, 3, 4):
+        for yd in (torch.float16, torch.float32):
+            fused = dm.gemv(p, gu, out_dtype=yd, silu_glu=True)
+            sep = dm.gemv(p, act, out_dtype=yd)
+            assert torch.equal(fused, sep)      # same f16 input bits -> same launch result
+    # and the separate path itself against the oracle on that input
+    a16 = m.scale_sets[3].alpha.astype(np.float16).astype(np.float32)
+    z16 = m.scale_sets[3].offset.astype(np.float16).astype(np.float32) if asym else None
+    want = O.gemv_lut(m.bitplanes.words, cols, 128, a16, z16, 3, act.float().cpu().numpy())
+    assert O.rel_dev(dm.gemv(3, gu, silu_glu=True).cpu().numpy(), want) <= NORTH_STAR_TOL
+    with pytest.raises(P.UsageError):
+        dm.gemv(3, gu.float(), silu_glu=True)
+    with pytest.raises(P.UsageError):
+        dm.gemv(3, gu[:cols], silu_glu=True)

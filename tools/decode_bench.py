@@ -20,6 +20,7 @@ ap.add_argument("--ctx", type=int, default=1024)
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--no-fp16", action="store_true")
+ap.add_argument("--ab-glu", action="store_true", help="also time the step with a separate silu_mul launch")
 ap.add_argument("--breakdown", action="store_true", help="also time the step without its linears")
 a = ap.parse_args()
 torch.cuda.set_device(0)
@@ -35,6 +36,10 @@ for p in a.p:
     out["anybcq"][f"p{p}"] = {"ms_per_token": round(ms, 4), "tokens_per_s": round(1e3 / ms, 1),
                               "weight_GB_per_token": round(gb / 1e9, 3),
                               "weight_GBps": round(gb / (ms * 1e-3) / 1e9, 1)}
+    if a.ab_glu:
+        qm.fuse_glu = False
+        out["anybcq"][f"p{p}"]["ms_per_token_separate_silu_mul"] = round(time_step(qm, a.iters), 4)
+        qm.fuse_glu = True
 if a.breakdown:  # the same step with the linears skipped: attention, norms, lm_head, ...
     import paper_2510_10467_b200.decode as D
     real_batch = D.gemv_batch

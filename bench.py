@@ -101,12 +101,13 @@ class ClockSampler:
         p = self.nvml
         while not self.stop.is_set():
             try:
+                ts = time.perf_counter()
                 sm = float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
                 try:
                     rs = int(p.nvmlDeviceGetCurrentClocksEventReasons(self.h))
                 except Exception:
                     rs = int(p.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
-                self.rows.append((sm, rs, time.perf_counter()))
+                self.rows.append((sm, rs, ts, time.perf_counter()))  # (query interval [ts, te])
             except Exception:
                 return
             time.sleep(0)  # (yield the GIL; the timed region can be only a few ms long)
@@ -131,11 +132,13 @@ class ClockSampler:
 
     def summary(self):
         t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
-        rows = [r for r in self.rows if t0 <= r[2] <= t1]
+        # a query counts when its interval overlaps the region (an NVML query can
+        # outlast a few-ms region, so 'completed inside' alone can find none)
+        rows = [r for r in self.rows if r[2] <= t1 and r[3] >= t0]
         if not rows:
             return self._smi_once()
         sm = [r[0] for r in rows]
-        reasons = sorted({n for _, rs, _ in rows for n, bit in self.REASONS.items() if rs & bit})
+        reasons = sorted({n for _, rs, _, _ in rows for n, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_sm, "reasons": reasons,
                 "samples": len(rows), "source": "nvml during the timed region"}
 
@@ -625,7 +628,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

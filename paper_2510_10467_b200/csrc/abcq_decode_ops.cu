@@ -288,9 +288,9 @@ __global__ void rope_attn_decode_fused(const __half* __restrict__ q, const __hal
     }
     __syncthreads();
     split_attend(qs[warp], ks, vs, n, scale, lane, part + ((size_t)h * splits + sp) * kPartStride);
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // the block's partial stores, then one gpu-scope fence (cumulative) + arrival
     if (threadIdx.x == 0) {
+        __threadfence();
         const unsigned prev = atomicAdd(&cnt[kh * 32], 1u);
         last = prev == (unsigned)splits - 1;
         if (last) cnt[kh * 32] = 0;  // self-reset for the next launch

@@ -519,3 +519,41 @@ def test_silu_glu_input_matches_separate_silu_mul(P, rows, cols, asym):
         dm.gemv(3, gu.float(), silu_glu=True)
     with pytest.raises(P.UsageError):
         dm.gemv(3, gu[:cols], silu_glu=True)
+
+
+def test_silu_glu_mixed_with_plain_jobs_in_one_batch(P):
+    """C-ABI batch: a SiLU-gated job next to plain f16 jobs (the gate is per job)."""
+    import ctypes as C
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.decode import silu_mul
+    L = _lib.lib()
+    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r + c), scale_dtype="f16")
+           for r, c in ((512, 1024), (256, 2048), (48, 1000))]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xs = [torch.randn(dms[0].cols, device="cuda", generator=g).half(),
+          (2 * torch.randn(2 * dms[1].cols, device="cuda", generator=g)).half(),   # [gate ; up]
+          torch.randn(dms[2].cols, device="cuda", generator=g).half()]
+    glu = [False, True, False]
+    ps = [3, 4, 2]
+    ys = [torch.empty(dm.rows, device="cuda", dtype=torch.float16) for dm in dms]
+    arr = (_lib.AbcqGemvJob * 3)()
+    for k, dm in enumerate(dms):
+        arr[k].model = C.pointer(dm._struct)
+        arr[k].p = ps[k]
+        arr[k].x_dtype = _lib.F16_SILU_GLU if glu[k] else _lib.F16
+        arr[k].y_dtype = _lib.F16
+        arr[k].x = xs[k].data_ptr()
+        arr[k].y = ys[k].data_ptr()
+    need = C.c_size_t()
+    _lib.check(L.abcq_gemv_batch_workspace_bytes(arr, 3, C.byref(need)))
+    ws = torch.zeros(max(int(need.value), 16), dtype=torch.uint8, device="cuda")
+    _lib.check(L.abcq_gemv_batch(arr, 3, ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream))
+    act = torch.empty(dms[1].cols, device="cuda", dtype=torch.float16)
+    silu_mul(xs[1][:dms[1].cols], xs[1][dms[1].cols:], act)
+    want = P.gemv_batch([(dms[0], 3, xs[0], torch.empty_like(ys[0])), (dms[1], 4, act, torch.empty_like(ys[1])),
+                         (dms[2], 2, xs[2], torch.empty_like(ys[2]))])
+    for k in range(3):
+        assert torch.equal(ys[k], want[k]), k
+    # an f32 job next to a gated one is rejected before any work
+    arr[0].x_dtype = _lib.F32
+    assert L.abcq_gemv_batch(arr, 3, ws.data_ptr(), ws.numel(), None) == _lib.E_ARG

@@ -250,7 +250,6 @@ __global__ void rope_attn_decode_fused(const __half* __restrict__ q, const __hal
                                        __half* __restrict__ vc, int heads, int kv_heads, int lmax, int pos,
                                        float scale, float* __restrict__ part, unsigned* __restrict__ cnt,
                                        __half* __restrict__ out) {
-    pdl_enter();
     constexpr int d = 128, h2 = d / 2;
     __shared__ __half ks[kAttnSplit][d + 2];
     __shared__ __align__(16) __half vs[kAttnSplit][d];
@@ -260,14 +259,18 @@ __global__ void rope_attn_decode_fused(const __half* __restrict__ q, const __hal
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = pos + 1, p0 = sp * kAttnSplit, n = min(kAttnSplit, L - p0);
     const int h = kh * g + warp;
+    const int rnew = pos - p0;  // the new token's row, if it lies in this split
+    // cache rows < pos are not the producer's output (q/k/v are): staged BEFORE
+    // the PDL wait, so on the SMs the previous grid's early CTAs free the KV
+    // reads overlap its tail
+    stage_kv<kAttnSplit>(kc, vc, kh, lmax, p0, n, rnew, ks, vs);
+    pdl_enter();
     for (int t = lane; t < h2; t += 32) {  // rope_append_kernel's expression, per query head
         const float x1 = __half2float(q[(size_t)h * d + t]), x2 = __half2float(q[(size_t)h * d + t + h2]);
         const float c = cosv[t], s = sinv[t];
         qs[warp][t] = __float2half_rn(x1 * c - x2 * s);
         qs[warp][t + h2] = __float2half_rn(x2 * c + x1 * s);
     }
-    const int rnew = pos - p0;  // the new token's row, if it lies in this split
-    stage_kv<kAttnSplit>(kc, vc, kh, lmax, p0, n, rnew, ks, vs);
     if (rnew >= 0 && rnew < n) {
         for (int t = threadIdx.x; t < h2; t += blockDim.x) {
             const float x1 = __half2float(k[(size_t)kh * d + t]), x2 = __half2float(k[(size_t)kh * d + t + h2]);

@@ -15,8 +15,10 @@ model would. The KV cache holds `ctx` positions of random keys/values and the
 step attends over all of them and writes position `ctx` (static shapes, so
 the whole step is captured in one CUDA graph).
 
-Per layer the quantized step issues 4 GEMV launches (abcq_gemv_batch):
-[q, k, v] (same x), [o], [gate, up] (same x), [down], plus the fused
+Per layer the quantized step issues 4 GEMV launches: q/k/v and gate/up are
+row-stacked models (BCQ scales are per row and group, so stacking is exact;
+`stack_rows=False` keeps them separate, one abcq_gemv_batch launch each),
+then [o] and [down], plus the fused
 harness ops of abcq_decode_ops.cu (add+RMSNorm x2, and RoPE + KV append +
 split-L decode attention + combine as ONE launch) -- the fp16 comparator uses
 the same fused ops. SiLU(gate)*up
@@ -123,14 +125,19 @@ class QuantizedLlamaStep:
     """Decode step with AnyBCQ linears at precision p (p_lo..p_hi resident)."""
 
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), p: int = 3, p_lo: int = 2, p_hi: int = 4,
-                 ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True):
-        self.cfg, self.p, self.fuse_glu = cfg, p, fuse_glu
+                 ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True, stack_rows: bool = True):
+        self.cfg, self.p, self.fuse_glu, self.stack_rows = cfg, p, fuse_glu, stack_rows
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.layers = []
         for _ in range(cfg.layers):
             mats = {}
-            for name, r, c in cfg.linear_shapes():
+            shapes = cfg.linear_shapes()
+            if stack_rows:  # q/k/v and gate/up as one row-stacked model each (BCQ is per row: exact)
+                sh = {n: (r, c) for n, r, c in shapes}
+                shapes = [("qkv", sh["q"][0] + sh["k"][0] + sh["v"][0], cfg.hidden), ("o",) + sh["o"],
+                          ("gu", 2 * cfg.intermediate, cfg.hidden), ("down",) + sh["down"]]
+            for name, r, c in shapes:
                 dm = DeviceModel(r, c, 128, p_lo, p_hi, False, scale_dtype="f16", device=self.device)
                 dm.load_planes(torch.randint(-2**31, 2**31 - 1, (p_hi, r, c // 32), dtype=torch.int32,
                                              device=self.device, generator=gen))
@@ -148,7 +155,8 @@ class QuantizedLlamaStep:
         hd, kvd, inter = cfg.hidden, cfg.kv_heads * cfg.head_dim, cfg.intermediate
         f16 = dict(device=self.device, dtype=torch.float16)
         self.x = torch.randn(hd, **f16, generator=gen)
-        self.q, self.k, self.v = torch.empty(hd, **f16), torch.empty(kvd, **f16), torch.empty(kvd, **f16)
+        self.qkv = torch.empty(hd + 2 * kvd, **f16)
+        self.q, self.k, self.v = self.qkv[:hd], self.qkv[hd:hd + kvd], self.qkv[hd + kvd:]
         self.o = torch.empty(hd, **f16)
         self.gu = torch.empty(2 * inter, **f16)   # [gate ; up]: the down GEMV's SiLU-gated input
         self.g, self.u = self.gu[:inter], self.gu[inter:]
@@ -166,12 +174,18 @@ class QuantizedLlamaStep:
         resid = None
         for li, mats in enumerate(self.layers):
             add_rmsnorm(self.x, resid, self.norm_w[li][0], self.h, cfg.eps)
-            gemv_batch([(mats["q"], p, self.h, self.q), (mats["k"], p, self.h, self.k),
-                        (mats["v"], p, self.h, self.v)])
+            if self.stack_rows:
+                mats["qkv"].gemv(p, self.h, out=self.qkv)
+            else:
+                gemv_batch([(mats["q"], p, self.h, self.q), (mats["k"], p, self.h, self.k),
+                            (mats["v"], p, self.h, self.v)])
             a = self.attn(li, self.q, self.k, self.v)
             mats["o"].gemv(p, a, out=self.o)
             add_rmsnorm(self.x, self.o, self.norm_w[li][1], self.h, cfg.eps)
-            gemv_batch([(mats["gate"], p, self.h, self.g), (mats["up"], p, self.h, self.u)])
+            if self.stack_rows:  # y = [gate ; up]: exactly the down GEMV's SiLU-gated input layout
+                mats["gu"].gemv(p, self.h, out=self.gu)
+            else:
+                gemv_batch([(mats["gate"], p, self.h, self.g), (mats["up"], p, self.h, self.u)])
             if self.fuse_glu:  # silu(gate)*up formed inside the down GEMV's table build
                 mats["down"].gemv(p, self.gu, out=self.d, silu_glu=True)
             else:

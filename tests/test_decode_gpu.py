@@ -110,3 +110,14 @@ def test_fused_rope_attention_equals_separate_launches(ctx):
         assert torch.equal(got, want)
         assert torch.equal(att.k_cache, kc1) and torch.equal(att.v_cache, vc1)
         assert torch.equal(qq, q) and torch.equal(kk, k)   # inputs left unrotated
+
+
+def test_quantized_step_separate_qkv_gateup_models():
+    from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    cfg = LlamaConfig(layers=2, vocab=1000)
+    m = QuantizedLlamaStep(cfg, p=2, ctx=64, stack_rows=False)
+    assert set(m.layers[0]) == {"q", "k", "v", "o", "gate", "up", "down"}
+    x0 = m.x.clone()
+    t1 = m.step().item()
+    m.x.copy_(x0)
+    assert m.step().item() == t1 and 0 <= t1 < 1000

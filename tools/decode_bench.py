@@ -20,6 +20,7 @@ ap.add_argument("--ctx", type=int, default=1024)
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--no-fp16", action="store_true")
+ap.add_argument("--ab-stack", action="store_true", help="also time separate q/k/v and gate/up models (batched)")
 ap.add_argument("--ab-glu", action="store_true", help="also time the step with a separate silu_mul launch")
 ap.add_argument("--breakdown", action="store_true", help="also time the step without its linears")
 a = ap.parse_args()
@@ -40,6 +41,13 @@ for p in a.p:
         qm.fuse_glu = False
         out["anybcq"][f"p{p}"]["ms_per_token_separate_silu_mul"] = round(time_step(qm, a.iters), 4)
         qm.fuse_glu = True
+if a.ab_stack:  # the same step with q/k/v and gate/up as separate models in one batched launch each
+    sm = QuantizedLlamaStep(cfg, p=a.p[0], ctx=a.ctx, stack_rows=False)
+    for p in a.p:
+        sm.p = p
+        out["anybcq"][f"p{p}"]["ms_per_token_unstacked"] = round(time_step(sm, a.iters), 4)
+    del sm
+    torch.cuda.empty_cache()
 if a.breakdown:  # the same step with the linears skipped: attention, norms, lm_head, ...
     import paper_2510_10467_b200.decode as D
     real_batch = D.gemv_batch

@@ -157,7 +157,7 @@ class ClockSampler:
 def make_layer_models(P, row_scale: int, copies: int, seed0: int = 0, p_lo: int = P_LO, p_hi: int = P_HI):
     """copies x 7 DeviceModels (p p_lo:p_hi, fp16 scales), synthetic planes/scales
     generated on the host from splitmix64."""
-    from oracle import anybcq_oracle as O  # synthetic-input generator only (not measured)
+    from paper_2510_10467_b200.tensor_io import random_words  # (the GPU leg never imports oracle/)
 
     models = []
     for c in range(copies):
@@ -166,7 +166,7 @@ def make_layer_models(P, row_scale: int, copies: int, seed0: int = 0, p_lo: int 
             rows = r * row_scale
             seed = seed0 + 1000 * c + li
             dm = P.DeviceModel(rows, k, 128, p_lo, p_hi, False, scale_dtype="f16")
-            dm.load_planes(O.random_words(p_hi, rows, k, seed=seed))
+            dm.load_planes(random_words(p_hi, rows, k, seed=seed))
             rng = np.random.default_rng(seed)
             for p in range(p_lo, p_hi + 1):
                 a = (0.01 + 0.1 * np.abs(rng.standard_normal((p, rows, k // 128)))).astype(np.float32)

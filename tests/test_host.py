@@ -90,3 +90,10 @@ def test_torch_ops_registered_and_trace_shapes():
         ops.model(h)
     with pytest.raises(P.UsageError):
         ops.register(object())
+
+
+def test_synthetic_words_match_the_oracle_generator():
+    from oracle import anybcq_oracle as O
+    from paper_2510_10467_b200.tensor_io import random_words
+    for planes, rows, cols, seed in ((4, 16, 4096, 3), (2, 5, 100, 7), (1, 3, 31, 0)):
+        assert np.array_equal(random_words(planes, rows, cols, seed), O.random_words(planes, rows, cols, seed))

@@ -385,12 +385,35 @@ def run_gpu(args):
                                                 stream), 5)
         p2g_us = per_sweep(lambda c: [gemv_batch([(pool[c][li], 2, xs[pool[c][li].cols], ys2[c][li]) for li in g],
                                                  stream) for g in DECODER_GROUPS], 5)
+        # decoder-grouped with q/k/v and gate/up as row-stacked AnyBCQ models (one
+        # GEMV per group, as the decode harness runs them; cuBLAS likewise on
+        # the concatenated fp16 weights) -- BCQ is per row and group: exact
+        from paper_2510_10467_b200.tensor_io import random_words
+        stacked = []
+        for c in range(5):
+            row = []
+            for gi, g in enumerate(DECODER_GROUPS):
+                r, k = sum(LAYERS[i][1] for i in g), LAYERS[g[0]][2]
+                dm = P.DeviceModel(r, k, 128, 2, 2, False, scale_dtype="f16")
+                dm.load_planes(random_words(2, r, k, seed=900 + 10 * c + gi))
+                dm.load_scale_set(2, (0.01 + 0.1 * np.abs(np.random.default_rng(c).standard_normal(
+                    (2, r, k // 128)))).astype(np.float32))
+                row.append(dm)
+            stacked.append(row)
+        ys_st = [torch.empty(m.rows, dtype=torch.float16, device=dev) for m in stacked[0]]
+        p2s_us = per_sweep(lambda c: [m.gemv(2, xs[m.cols], out=ys_st[gi], stream=stream)
+                                      for gi, m in enumerate(stacked[c])], 5)
+        del stacked
         fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)
         fp16 = {"us_per_sweep": round(fp16_us, 2), "GBps": round(fp16_bytes / (fp16_us * 1e-6) / 1e9, 1),
                 "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2),
                 "abcq_p2_batched_us_per_sweep": round(p2b_us, 2), "speedup_p2_batched": round(fp16_us / p2b_us, 2),
                 "decoder_grouped": {"cublas_fp16_us": round(fp16g_us, 2), "abcq_p2_us": round(p2g_us, 2),
                                     "speedup_p2": round(fp16g_us / p2g_us, 2),
+                                    "abcq_p2_stacked_us": round(p2s_us, 2),
+                                    "speedup_p2_stacked": round(fp16g_us / p2s_us, 2),
+                                    "stacked": "q/k/v and gate/up as one row-stacked AnyBCQ model each "
+                                               "(4 single GEMVs per sweep, as tools/decode_bench.py runs them)",
                                     "launches": "4 per sweep each: [q,k,v] [o] [gate,up] [down] (cuBLAS on "
                                                 "concatenated fp16 weights)"},
                 "note": "7 layers at p=2 vs fp16: cuBLAS 7 torch.mv; abcq 7 single launches / 1 gemv_batch / "

@@ -496,7 +496,7 @@ def test_torch_ops_match_device_model(P):
 # --- SiLU-gated input (ABCQ_F16_SILU_GLU): silu(g)*u formed in the table build ----
 
 @pytest.mark.parametrize("rows,cols,asym", [(4096, 14336, False), (256, 1024, True), (37, 200, False),
-                                            (48, 1000, True)])
+                                            (48, 1000, True), (37, 1001, False), (20, 333, True)])
 def test_silu_glu_input_matches_separate_silu_mul(P, rows, cols, asym):
     from paper_2510_10467_b200.decode import silu_mul
     m = synth_model(P, rows, cols, 2, 4, asym=asym, seed=rows ^ cols)

@@ -92,9 +92,16 @@ int abcq_device_check(int32_t dev);
  * u64 %globaltimer stamps per CTA (phases: start, prefetch issued, PDL wait
  * done, table built, stream done, reduction done) to d_buf[cta*8 + k].    */
 int abcq_debug_set_trace(void* d_buf);
-/* profiling experiments only (results are WRONG when mode != 0): 1 = skip
- * the table lookups, 2 = skip the weight loads. Default 0.                */
+/* profiling experiments only (results are WRONG when mode is 1 or 2): 1 =
+ * skip the table lookups, 2 = skip the weight loads; 23 = route single GEMVs
+ * through the batch kernel instead of the cluster kernel; 5000 + 100*slots +
+ * 10*C + t = force the cluster kernel's geometry (5000 = automatic). Default 0. */
 int abcq_debug_set_mode(int32_t mode);
+/* profiling aid: the launch geometry a single GEMV (abcq_gemv, or a batch of
+ * one job) uses for this model and precision -- out7 = {cluster size C,
+ * clusters M, CTAs per SM, tiles per stage, ring slots, stage bytes, dynamic
+ * shared-memory bytes}; ABCQ_E_LAYOUT when the call takes another kernel.  */
+int abcq_debug_gemv_geometry(const abcq_model_t* m, int32_t p, int32_t* out7);
 
 /* ---- layout sizes (host-only arithmetic) ---------------------------------
  * Tiled layout: 16-row tiles x 256-column slices; see DESIGN.md §Layout.  */

@@ -50,6 +50,8 @@ int check_call(const abcq_model_t* m, int p, const void* x, int xd, const void* 
     if (m->asymmetric && !m->offset[p]) return fail(ABCQ_E_ARG, "offset set %d missing", p);
     if (!x || !y) return fail(ABCQ_E_ARG, "x / y pointer is NULL");
     if (!(dtype_ok(xd) || xd == ABCQ_F16_SILU_GLU) || !dtype_ok(yd)) return fail(ABCQ_E_ARG, "bad x/y dtype");
+    if (m->layout == ABCQ_LAYOUT_TILED && ((uintptr_t)x & 15u))
+        return fail(ABCQ_E_ARG, "x must be 16-byte aligned for the tiled-layout kernels (got %p)", x);
     if (xd == ABCQ_F16_SILU_GLU && !abcq::lut_supports(m, p))
         return fail(ABCQ_E_LAYOUT, "the SiLU-gated x dtype needs the tiled layout (group 128)");
     return 0;
@@ -75,6 +77,10 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
+    if (mode >= 5000 && mode < 6000) {  // cluster GEMV geometry: 5000 + 100*slots + 10*C + tiles/warp (5000 = auto)
+        abcq::g_cl_force = mode - 5000;
+        return 0;
+    }
     if (mode >= 3000) {  // CTA partition strategy
         abcq::g_partition = mode - 3000;
         return 0;
@@ -97,6 +103,14 @@ int abcq_debug_set_trace(void* d_buf) {
 }
 
 const char* abcq_last_error(void) { return g_err; }
+
+int abcq_debug_gemv_geometry(const abcq_model_t* m, int32_t p, int32_t* out7) {
+    if (int rc = check_model(m)) return rc;
+    if (!out7) return fail(ABCQ_E_ARG, "out is NULL");
+    if (abcq::gemv_cluster_geometry(m, p, out7) != 0)
+        return fail(ABCQ_E_LAYOUT, "no cluster geometry for this model / precision");
+    return 0;
+}
 
 int abcq_device_check(int32_t dev) {
     cudaDeviceProp prop;
@@ -173,6 +187,9 @@ int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes) {
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y, int32_t y_dtype,
               void* d_workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_call(m, p, d_x, x_dtype, d_y, y_dtype)) return rc;
+    if (abcq::cluster_supports(m, p))  // single GEMV: no workspace
+        return cuda_ret(abcq::launch_gemv_cluster(m, p, d_x, x_dtype, d_y, y_dtype, (cudaStream_t)stream),
+                        "abcq_gemv");
     if (abcq::lut_supports(m, p)) {
         const size_t need = abcq::lut_workspace_bytes(m);
         if (need && (!d_workspace || workspace_bytes < need))

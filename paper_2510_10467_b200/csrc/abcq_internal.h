@@ -27,6 +27,13 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                      int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st);
 int lut_max_jobs();
 
+// single GEMV through the cluster kernel (abcq_gemv_cluster.cu): no workspace
+bool cluster_supports(const abcq_model_t* m, int p);
+int launch_gemv_cluster(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
+                        cudaStream_t st);
+int gemv_cluster_geometry(const abcq_model_t* m, int p, int* out7);
+extern int g_cl_force;
+
 // small-batch mixed-precision GEMM (tensor cores), B <= 16
 size_t gemm_workspace_bytes(const abcq_model_t* m, int B);
 int launch_gemm_mixedp(const abcq_model_t* m, int B, const int* p_host, const void* x, void* y, int y_dtype,

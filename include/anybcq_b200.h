@@ -200,9 +200,12 @@ int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype
  *   rope_attn_decode: rope_append + attn_decode over [0, pos] in ONE launch,
  *                bitwise equal to that pair; q and k are left unrotated (only
  *                the cache row pos receives the rotated k). The workspace
- *                (abcq_attn_decode_workspace_bytes(heads, pos + 1)) must be
- *                zero-filled once before first use: it holds self-resetting
- *                per-kv-head counters (the last split block combines)
+ *                (abcq_attn_decode_workspace_bytes(heads, ctx) with ctx >= pos + 1,
+ *                e.g. sized once for max_ctx) must be zero-filled once before
+ *                first use: it starts with self-resetting per-head counters
+ *                (the last split block combines) at a fixed offset, so one
+ *                workspace serves every pos, in any order, and the separate
+ *                attn_decode path
  *   silu_mul:    a = silu(g) * u                                            */
 int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
                          void* stream);

@@ -100,7 +100,7 @@ def build_parser() -> argparse.ArgumentParser:
     b.add_argument("--bits", default="all")
     b.add_argument("--repeats", type=int, default=32)
     b.add_argument("--seed", type=int, default=0)
-    b.add_argument("--dense", action="store_true", help="add the fp16 cuBLAS GEMV row")
+    b.add_argument("--dense", action="store_true", help="add the dense f32 GEMV row (reference contract)")
     b.add_argument("--format", choices=("text", "csv"), default="text")
     b.set_defaults(func=_cmd_bench)
     return ap

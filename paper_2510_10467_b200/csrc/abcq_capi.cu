@@ -224,7 +224,7 @@ static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {
 int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n, size_t* out_bytes) {
     if (int rc = check_jobs(jobs, n)) return rc;
     if (!out_bytes) return fail(ABCQ_E_ARG, "out_bytes is NULL");
-    const abcq_model_t* models[32];
+    const abcq_model_t* models[abcq::kMaxBatchJobs];
     for (int j = 0; j < n; ++j) models[j] = jobs[j].model;
     *out_bytes = abcq::lut_jobs_workspace_bytes(models, n);
     return 0;
@@ -235,11 +235,11 @@ int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t w
     if (int rc = abcq_gemv_batch_workspace_bytes(jobs, n, &need)) return rc;
     if (need && (!d_ws || ws_bytes < need))
         return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
-    const abcq_model_t* models[ABCQ_MAX_PLANES + 16];
-    int ps[ABCQ_MAX_PLANES + 16];
-    const void* xs[ABCQ_MAX_PLANES + 16];
-    void* ys[ABCQ_MAX_PLANES + 16];
-    int xds[ABCQ_MAX_PLANES + 16];
+    const abcq_model_t* models[abcq::kMaxBatchJobs];
+    int ps[abcq::kMaxBatchJobs];
+    const void* xs[abcq::kMaxBatchJobs];
+    void* ys[abcq::kMaxBatchJobs];
+    int xds[abcq::kMaxBatchJobs];
     for (int j = 0; j < n; ++j) {
         xds[j] = jobs[j].x_dtype;
         models[j] = jobs[j].model;

@@ -359,20 +359,23 @@ int launch_rope_append(void* q, void* k, const void* v, const float* cosv, const
                            static_cast<__half*>(kc), static_cast<__half*>(vc), heads, kv_heads, d, lmax, pos);
 }
 
-// partials, then one counter per kv head on its own 128-byte line (fused kernel)
+// workspace: one counter per head on its own 128-byte line (fused kernel;
+// zero-filled once, self-resetting) at a FIXED offset 0 -- independent of the
+// position, so one workspace serves every pos / ctx -- then the partials
+size_t attn_decode_counter_bytes(int heads) { return (size_t)heads * 32 * sizeof(unsigned); }
 size_t attn_decode_part_bytes(int heads, int L) {
     return (size_t)heads * ((L + kAttnSplit - 1) / kAttnSplit) * kPartStride * sizeof(float);
 }
 size_t attn_decode_workspace_bytes(int heads, int L) {
-    return attn_decode_part_bytes(heads, L) + (size_t)heads * 32 * sizeof(unsigned);
+    return attn_decode_counter_bytes(heads) + attn_decode_part_bytes(heads, L);
 }
 
 int launch_rope_attn_decode(const void* q, const void* k, const void* v, const float* cosv, const float* sinv,
                             void* kc, void* vc, int heads, int kv_heads, int lmax, int pos, float scale, void* out,
                             void* ws, cudaStream_t st) {
     const int splits = (pos + 1 + kAttnSplit - 1) / kAttnSplit;
-    float* part = static_cast<float*>(ws);
-    unsigned* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + attn_decode_part_bytes(heads, pos + 1));
+    unsigned* cnt = static_cast<unsigned*>(ws);
+    float* part = reinterpret_cast<float*>(static_cast<char*>(ws) + attn_decode_counter_bytes(heads));
     return (int)launch_pdl(rope_attn_decode_fused, dim3(kv_heads, splits), dim3(32 * (heads / kv_heads)), st,
                            static_cast<const __half*>(q), static_cast<const __half*>(k),
                            static_cast<const __half*>(v), cosv, sinv, static_cast<__half*>(kc),
@@ -386,10 +389,11 @@ int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads,
     cudaError_t e = launch_pdl(attn_decode_partial, dim3(kv_heads, splits), dim3(32 * (heads / kv_heads)), st,
                                static_cast<const __half*>(q), static_cast<const __half*>(kc),
                                static_cast<const __half*>(vc), heads, kv_heads, lmax, L, scale,
-                               static_cast<float*>(ws));
+                               reinterpret_cast<float*>(static_cast<char*>(ws) + attn_decode_counter_bytes(heads)));
     if (e != cudaSuccess) return (int)e;
-    return (int)launch_pdl(attn_decode_combine, dim3(heads), dim3(128), st, static_cast<const float*>(ws), splits,
-                           static_cast<__half*>(out));
+    return (int)launch_pdl(attn_decode_combine, dim3(heads), dim3(128), st,
+                           reinterpret_cast<const float*>(static_cast<const char*>(ws) + attn_decode_counter_bytes(heads)),
+                           splits, static_cast<__half*>(out));
 }
 
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st) {

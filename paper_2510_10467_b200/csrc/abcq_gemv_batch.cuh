@@ -22,7 +22,7 @@
 
 namespace abcq {
 
-constexpr int kMaxJobs = 32;
+constexpr int kMaxJobs = kMaxBatchJobs;
 constexpr int kWarps = 16;
 constexpr int kBThreads = kWarps * 32;
 

@@ -9,6 +9,8 @@
 
 namespace abcq {
 
+constexpr int kMaxBatchJobs = 32;  // jobs per abcq_gemv_batch launch (abcq_gemv_batch_max_jobs)
+
 int launch_pack_planes(const uint32_t* words, int planes, int rows, int cols, void* out, cudaStream_t st);
 int launch_unpack_planes(const void* tiled, int planes, int rows, int cols, uint32_t* words, cudaStream_t st);
 int launch_pack_scales(const float* alpha, const float* offset, int p, int rows, int cols, int scale_dtype,

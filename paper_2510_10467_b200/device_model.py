@@ -12,6 +12,7 @@ model_format.py:1-15).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 import torch
@@ -203,11 +204,16 @@ class DeviceModel:
 
     def _order_after_upload(self, p: int, stream) -> None:
         ev = self._level_ready.get(p)
-        if ev is None or torch.cuda.is_current_stream_capturing():
-            return  # (CUDA graphs are captured once the model is resident)
+        if ev is None:
+            return
         if ev.query():  # upload finished: no ordering needed from now on
             del self._level_ready[p]
             return
+        if torch.cuda.is_current_stream_capturing():
+            # a graph captured now would replay reads of planes / scales that
+            # have not landed (the kernels prefetch weights before their PDL wait)
+            raise UsageError(f"precision {p} is still uploading; capture CUDA graphs once the model is "
+                             "resident (synchronize the upload first)")
         (stream if stream is not None else torch.cuda.current_stream(self.device)).wait_event(ev)
 
     def struct_ptr(self):
@@ -320,7 +326,7 @@ class DeviceModel:
 
 
 _BATCH_WS: dict = {}
-_BATCH_PLAN: dict = {}  # job-list key -> (ctypes job array, workspace, models)
+_BATCH_PLAN: dict = {}  # job-list key -> (ctypes job array, workspace, weak refs to the models)
 
 
 def gemv_batch(jobs, stream=None):
@@ -348,10 +354,13 @@ def gemv_batch(jobs, stream=None):
                       out.data_ptr(), out.dtype, out.numel(), out.is_contiguous())
                      for dm, p, x, out in jobs))
     hit = _BATCH_PLAN.get(pkey)
-    if hit is not None and not any(dm._level_ready for dm, _, _, _ in jobs):
-        arr, ws, _models = hit
-        _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
-        return [j[3] for j in jobs]
+    if hit is not None:
+        arr, ws, refs = hit
+        if not all(r() is j[0] for r, j in zip(refs, jobs)):  # a model died; its id() was reused
+            del _BATCH_PLAN[pkey]
+        elif not any(dm._level_ready for dm, _, _, _ in jobs):
+            _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
+            return [j[3] for j in jobs]
     arr = (_lib.AbcqGemvJob * n)()
     keep = []
     for k, (dm, p, x, out) in enumerate(jobs):
@@ -379,9 +388,14 @@ def gemv_batch(jobs, stream=None):
         _BATCH_WS[key] = ws
     _lib.check(L.abcq_gemv_batch(arr, n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
     if all(j[2].is_contiguous() for j in jobs):
-        if len(_BATCH_PLAN) > 256:
-            _BATCH_PLAN.clear()
-        _BATCH_PLAN[pkey] = (arr, ws, [j[0] for j in jobs])  # (models kept alive: id() stays unique)
+        if len(_BATCH_PLAN) > 256:  # drop lists whose models are gone, then everything
+            for k in [k for k, v in _BATCH_PLAN.items() if any(r() is None for r in v[2])]:
+                del _BATCH_PLAN[k]
+            if len(_BATCH_PLAN) > 256:
+                _BATCH_PLAN.clear()
+        # models held by weak references: a cached job list never keeps a
+        # model's device memory alive; a hit re-checks identity (id() reuse)
+        _BATCH_PLAN[pkey] = (arr, ws, [weakref.ref(j[0]) for j in jobs])
     return [j[3] for j in jobs]
 
 

@@ -203,9 +203,14 @@ def _time_device(fn, repeats: int, warmup: int = 1, inner: int = 8) -> tuple[flo
 
 
 def bench(model, precisions, x, repeats: int = 32, paths=("naive", "lut"),
-          include_dense: bool = False, dense_weights=None) -> list[BenchRow]:
+          include_dense: bool = False, dense_weights=None, include_dense_f16: bool = False) -> list[BenchRow]:
     """Median/min device latency per (path, precision) with exact counters.
-    The 'dense' row is the cuBLAS half-precision GEMV of the p_hi weights."""
+
+    include_dense: the reference's dense row ("dense", 32, rows*cols*4) --
+    the f32 GEMV of the p_hi weights (dequantized, or `dense_weights`), here a
+    cuBLAS f32 matvec (gemv.py:335-344). include_dense_f16: an extra
+    ("dense_f16", 16, rows*cols*2) row, the cuBLAS half-precision GEMV the
+    north star compares against."""
     if repeats < 1:
         raise UsageError("repeats must be >= 1")
     for path in paths:
@@ -225,14 +230,18 @@ def bench(model, precisions, x, repeats: int = 32, paths=("naive", "lut"),
                 st = engine._stats(p, 0, 0.0)
                 out.append(BenchRow(rows, cols, path, p, med, lo, st.plane_bytes_fetched,
                                     st.scale_bytes_fetched))
-        if include_dense:
+        if include_dense or include_dense_f16:
             if dense_weights is None:
-                wh = dm.dequantize(model.p_hi, torch.float16)
+                wf = dm.dequantize(model.p_hi, torch.float32)
             else:
-                wh = torch.as_tensor(np.asarray(dense_weights, dtype=np.float32)).to(dm.device).half()
-            xh = xd.half()
+                wf = torch.as_tensor(np.asarray(dense_weights, dtype=np.float32)).to(dm.device)
+        if include_dense:
+            med, lo = _time_device(lambda: torch.mv(wf, xd), repeats)
+            out.append(BenchRow(rows, cols, "dense", 32, med, lo, rows * cols * 4, 0))
+        if include_dense_f16:
+            wh, xh = wf.half(), xd.half()
             med, lo = _time_device(lambda: torch.mv(wh, xh), repeats)
-            out.append(BenchRow(rows, cols, "dense", 16, med, lo, rows * cols * 2, 0))
+            out.append(BenchRow(rows, cols, "dense_f16", 16, med, lo, rows * cols * 2, 0))
     return out
 
 

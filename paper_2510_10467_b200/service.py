@@ -14,7 +14,8 @@ request/response fields and status codes mirror the reference's:
     POST /models/{name}/gemv        {precision, x, path}    -> {precision, path, y, stats}
     POST /models/{name}/bench       {precisions, repeats, include_dense, seed} -> {rows, cols, results}
 
-UsageError -> 400, missing model -> 404, container problems -> 422. The
+UsageError -> 400, missing model -> 404, container problems (FileFormatError)
+-> 500 with the reason, as upstream (server.py:111-117). The
 quantize / refine / matrix-upload endpoints are out of scope.
 
     uvicorn paper_2510_10467_b200.service:app
@@ -110,8 +111,8 @@ class ModelStore:
             raw = fh.read()
         try:
             lay = read_layout(raw, path)
-        except FileFormatError as exc:
-            raise HTTPException(422, str(exc))
+        except FileFormatError as exc:  # stored artifact unreadable: 500 with the reason (server.py:114-117)
+            raise HTTPException(500, str(exc))
         return ModelInfo(name=name, rows=lay.rows, cols=lay.cols, bits_lo=lay.p_lo, bits_hi=lay.p_hi,
                          group_size=lay.group_size, mode=lay.mode)
 
@@ -130,7 +131,7 @@ class ModelStore:
             try:
                 dm = ProgressiveLoader(path).load_all()
             except FileFormatError as exc:
-                raise HTTPException(422, str(exc))
+                raise HTTPException(500, str(exc))
             eng = GemvEngine(dm)
             self._cache[name] = (mtime, eng)
             return eng
@@ -140,6 +141,10 @@ def create_app(home: str | os.PathLike | None = None) -> FastAPI:
     store = ModelStore(Path(home or os.environ.get("ANYBCQ_HOME", "./anybcq_home")))
     app = FastAPI(title="anybcq-b200", version=__version__)
     app.state.store = store
+    # /bench captures CUDA graphs; a concurrent /gemv's blocking copies and
+    # allocations would invalidate the capture (or fail under it): device work
+    # of the two endpoints is serialised (GEMV requests are microseconds)
+    gpu_lock = threading.Lock()
 
     @app.get("/health")
     def health():
@@ -158,7 +163,8 @@ def create_app(home: str | os.PathLike | None = None) -> FastAPI:
         engine = store.engine(name)
         try:
             run = engine.lut if req.path == "lut" else engine.naive
-            y, st = run(req.precision, req.x)
+            with gpu_lock:
+                y, st = run(req.precision, req.x)
         except UsageError as exc:
             raise HTTPException(400, str(exc))
         return GemvResponse(precision=req.precision, path=req.path, y=[float(v) for v in y],
@@ -177,7 +183,8 @@ def create_app(home: str | os.PathLike | None = None) -> FastAPI:
         precisions = req.precisions or list(dm.precisions)
         x = random_gaussian(1, dm.cols, req.seed).ravel()
         try:
-            rows = bench(dm, precisions, x, repeats=req.repeats, include_dense=req.include_dense)
+            with gpu_lock:
+                rows = bench(dm, precisions, x, repeats=req.repeats, include_dense=req.include_dense)
         except UsageError as exc:
             raise HTTPException(400, str(exc))
         return BenchResponse(rows=dm.rows, cols=dm.cols, results=[

@@ -178,7 +178,7 @@ def test_service_registry(tmp_path):
     assert info == {"name": "small", "rows": 64, "cols": 256, "bits_lo": 2, "bits_hi": 3,
                     "group_size": 128, "mode": "symmetric"}
     assert client.get("/models/nope").status_code == 404
-    assert client.get("/models/broken").status_code == 422
+    assert client.get("/models/broken").status_code == 500   # FileFormatError, as upstream (server.py:114-117)
     assert client.post("/models/nope/gemv", json={"precision": 2, "x": [0.0]}).status_code == 404
     assert client.post("/models/small/gemv", json={"precision": 99, "x": [0.0]}).status_code == 422
     assert client.post("/models/small/gemv",

@@ -83,7 +83,7 @@ def test_cli_bench_runs(capsys):
     out = capsys.readouterr().out.strip().splitlines()
     assert out[0] == "shape,path,p,median_us,plane_bytes,scale_bytes"
     assert {tuple(r.split(",")[1:3]) for r in out[1:]} >= {("lut", "2"), ("lut", "3"), ("naive", "2"),
-                                                            ("dense", "16")}
+                                                            ("dense", "32")}
 
 
 def test_service_gemv_per_request_precision(tmp_path):

@@ -121,3 +121,89 @@ def test_quantized_step_separate_qkv_gateup_models():
     t1 = m.step().item()
     m.x.copy_(x0)
     assert m.step().item() == t1 and 0 <= t1 < 1000
+
+
+def test_fused_attention_workspace_reused_across_positions():
+    """One workspace (sized once for the largest context) serves the fused
+    RoPE + attention kernel at decreasing and increasing positions: the
+    per-head counters sit at a fixed offset, so every call
+    completes and matches the separate launches bitwise."""
+    import ctypes as C
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.decode import LlamaConfig, _rope_tables
+    cfg = LlamaConfig(layers=1)
+    L = _lib.lib()
+    lmax = 1025
+    g = torch.Generator(device="cuda").manual_seed(11)
+    shape = (cfg.kv_heads, lmax, cfg.head_dim)
+    kc0 = torch.randn(shape, device="cuda", dtype=torch.float16, generator=g)
+    vc0 = torch.randn(shape, device="cuda", dtype=torch.float16, generator=g)
+    n = C.c_size_t()
+    _lib.check(L.abcq_attn_decode_workspace_bytes(cfg.heads, lmax, C.byref(n)))
+    ws = torch.zeros(int(n.value), dtype=torch.uint8, device="cuda")      # shared by every fused call
+    ws_sep = torch.zeros(int(n.value), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    scale = 1.0 / math.sqrt(cfg.head_dim)
+    for pos in (1024, 300, 63, 64, 0, 700, 5):
+        q = torch.randn(cfg.hidden, device="cuda", generator=g).half()
+        k = torch.randn(1024, device="cuda", generator=g).half()
+        v = torch.randn(1024, device="cuda", generator=g).half()
+        cos, sin = _rope_tables(cfg, pos, "cuda")
+        kc, vc = kc0.clone(), vc0.clone()
+        out = torch.empty(cfg.hidden, device="cuda", dtype=torch.float16)
+        _lib.check(L.abcq_rope_attn_decode_f16(q.data_ptr(), k.data_ptr(), v.data_ptr(), cos.data_ptr(),
+                                               sin.data_ptr(), kc.data_ptr(), vc.data_ptr(), cfg.heads, cfg.kv_heads,
+                                               lmax, pos, scale, out.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        kc2, vc2, q2, k2 = kc0.clone(), vc0.clone(), q.clone(), k.clone()
+        want = torch.empty_like(out)
+        _lib.check(L.abcq_rope_append_f16(q2.data_ptr(), k2.data_ptr(), v.data_ptr(), cos.data_ptr(), sin.data_ptr(),
+                                          kc2.data_ptr(), vc2.data_ptr(), cfg.heads, cfg.kv_heads, cfg.head_dim,
+                                          lmax, pos, st))
+        _lib.check(L.abcq_attn_decode_f16(q2.data_ptr(), kc2.data_ptr(), vc2.data_ptr(), cfg.heads, cfg.kv_heads,
+                                          lmax, pos + 1, scale, want.data_ptr(), ws_sep.data_ptr(), ws_sep.numel(),
+                                          st))
+        torch.cuda.synchronize()
+        assert torch.equal(out, want), pos
+        assert torch.equal(kc, kc2) and torch.equal(vc, vc2), pos
+
+
+class _DenseGemv:
+    """A linear with the dense weights abcq_dequantize reconstructs (bcq.py:372-378),
+    applied in fp32 by torch -- the reference for one AnyBCQ GEMV of the step."""
+
+    def __init__(self, dm, p):
+        self.w = dm.dequantize(p)            # (rows, cols) f32 on the device
+        self.cols = dm.cols
+
+    def gemv(self, p, x, out=None, silu_glu=False):
+        if silu_glu:
+            g, u = x[:self.cols].float(), x[self.cols:].float()
+            x = (torch.nn.functional.silu(g) * u).half()   # the f16 input the fused GEMV forms
+        y = self.w @ x.float()
+        out.copy_(y.to(out.dtype))
+        return out
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_quantized_step_matches_dense_dequantized_step(p):
+    """A 2-layer Llama-3-8B-shaped decode step with every linear an AnyBCQ GEMV
+    vs the same step with the dense weights abcq_dequantize reconstructs (fp32
+    torch matmuls, the same f16 rounding points): residual stream and final
+    hidden state agree to f16 rounding."""
+    from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    cfg = LlamaConfig(layers=2, vocab=1000)
+    m = QuantizedLlamaStep(cfg, p=p, ctx=64)
+    x0 = m.x.clone()
+    k0, v0 = m.attn.k_cache.clone(), m.attn.v_cache.clone()
+    m.step()
+    x_q, h_q = m.x.float().clone(), m.h.float().clone()
+    dense = [{name: _DenseGemv(dm, p) for name, dm in mats.items()} for mats in m.layers]
+    m.layers = dense
+    m.x.copy_(x0)
+    m.attn.k_cache.copy_(k0)
+    m.attn.v_cache.copy_(v0)
+    m.step()
+    x_d, h_d = m.x.float(), m.h.float()
+    rel = lambda a, b: float((a - b).norm() / b.norm())  # noqa: E731
+    assert rel(x_q, x_d) <= 1e-2, rel(x_q, x_d)
+    assert rel(h_q, h_d) <= 1e-2, rel(h_q, h_d)

@@ -116,6 +116,39 @@ def test_engine_matches_reference_outputs(P, name):
                     assert np.all(y == 0.0) and np.all(yn == 0.0)   # test_gemv.py:104-109
 
 
+@pytest.mark.parametrize("name", ["g128_64x256", "asym_g40_16x80", "g128_ragged_37x200"])
+def test_module_level_gemv_lut_and_naive(P, name):
+    """gemv_lut / gemv_naive (gemv.py:253-258): a fresh engine per call, the
+    reference's outputs, counters and chunk-width validation."""
+    c = load_case(name)
+    model = make_model(P, c)
+    x = c["x_0"]
+    for p in model.precisions:
+        for mu in (4, 8):
+            y, st = P.gemv_lut(model, p, x, chunk_width=mu)
+            assert O.rel_dev(y, c.get(f"lut{mu}_p{p}_x0", c[f"lut8_p{p}_x0"])) <= REF_TOL
+            assert st.lut_build_count == 1
+        yn, stn = P.gemv_naive(model, p, x)
+        assert O.rel_dev(yn, c[f"naive_p{p}_x0"]) <= REF_TOL
+        assert stn.lut_build_count == 0 and stn.plane_bytes_fetched == st.plane_bytes_fetched
+    with pytest.raises(P.UsageError):
+        P.gemv_lut(model, model.p_lo, x, chunk_width=5)
+    with pytest.raises(P.UsageError):
+        P.gemv_naive(model, model.p_hi + 1, x)
+
+
+def test_misaligned_x_rejected(P):
+    """A contiguous but misaligned x view (storage offset) is a usage error
+    before any launch -- not a misaligned-address fault."""
+    m = synth_model(P, 64, 256, 2, 3, seed=4)
+    dm = P.DeviceModel.from_model(m, scale_dtype="f16")
+    buf = torch.randn(257, device="cuda").half()
+    with pytest.raises(P.UsageError):
+        dm.gemv(2, buf[1:])
+    y = dm.gemv(2, buf[1:].clone())     # an aligned copy works
+    assert torch.isfinite(y).all()
+
+
 def test_single_active_column(P):
     c = load_case("single_col_1x4")                                    # test_gemv.py:94-101
     eng = P.GemvEngine(make_model(P, c))
@@ -258,6 +291,10 @@ def test_bench_counters_and_render(P):
     rows = P.bench(make_model(P, c), [2, 4], c["x_0"], repeats=3, include_dense=True)
     by = {(r.path, r.precision): r for r in rows}
     assert by[("lut", 2)].plane_bytes * 2 == by[("lut", 4)].plane_bytes
+    assert by[("dense", 32)].plane_bytes == 32 * 128 * 4     # the reference's dense row (gemv.py:344)
+    assert ("dense_f16", 16) not in by
+    rows16 = P.bench(make_model(P, c), [2], c["x_0"], repeats=2, include_dense_f16=True)
+    assert {(r.path, r.precision): r for r in rows16}[("dense_f16", 16)].plane_bytes == 32 * 128 * 2
     csv = P.render_bench_csv(rows)
     assert csv.splitlines()[0] == "shape,path,p,median_us,plane_bytes,scale_bytes"
     assert len(csv.splitlines()) == len(rows) + 1
@@ -459,6 +496,25 @@ def test_gemm_mixedp_matches_per_request_oracle(P, rows, cols, asym):
             z16 = None if z is None else z.astype(np.float16).astype(np.float32)
             want = O.gemv_lut(m.bitplanes.words, cols, 128, a16, z16, p, Xh[b])
             assert O.rel_dev(Y[b], want) <= 1e-4, (B, b, p, O.rel_dev(Y[b], want))
+
+
+@pytest.mark.parametrize("asym", [False, True])
+def test_gemm_mixedp_mlp_shape_b16_vs_c_oracle(P, asym):
+    """The Llama-3-8B gate/up shape (14336x4096) at B = 16 mixed precisions
+    (BASELINE config 3) vs the C oracle, per request."""
+    from oracle import c_oracle
+    rows, cols = 14336, 4096
+    m = synth_model(P, rows, cols, 2, 4, asym=asym, seed=77)
+    dm = P.DeviceModel.from_model(m, scale_dtype="f16")
+    ps = [2 + b % 3 for b in range(16)]
+    X = np.stack([O.random_gaussian(1, cols, seed=300 + b).ravel() for b in range(16)])
+    Xh = X.astype(np.float16).astype(np.float32)
+    Y = dm.gemm_mixedp(ps, torch.from_numpy(Xh).cuda()).cpu().numpy()
+    for b, p in enumerate(ps):
+        a16 = m.scale_sets[p].alpha.astype(np.float16).astype(np.float32)
+        z16 = m.scale_sets[p].offset.astype(np.float16).astype(np.float32) if asym else None
+        want = c_oracle.lut_gemv(m.bitplanes.words, cols, 128, a16, z16, p, Xh[b], threads=c_oracle.cpu_threads())
+        assert O.rel_dev(Y[b], want) <= 1e-4, (b, p, O.rel_dev(Y[b], want))
 
 
 @pytest.mark.parametrize("asym", [False, True])

@@ -175,7 +175,7 @@ class BenchRow:
     scale_bytes: int
 
 
-def _time_device(fn, repeats: int, warmup: int = 1, inner: int = 8) -> tuple[float, float]:
+def _time_device(fn, repeats: int, warmup: int = 1, inner: int = 32) -> tuple[float, float]:
     """Median/min device microseconds per call; each sample times `inner`
     back-to-back launches between CUDA events so host enqueue gaps do not
     count (the reference times single calls with perf_counter, gemv.py:296-305)."""

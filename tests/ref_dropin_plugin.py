@@ -1,0 +1,56 @@
+"""pytest plugin: route the reference package's GEMV engine to this repo's
+drop-in before the reference's own test modules import it.
+
+Loaded with `-p ref_dropin_plugin` by tests/test_reference_suite_gpu.py, which
+runs the reference's unchanged test files (installed under baseline/_ref by
+tools/install_reference.sh) on the B200 engine. This is the reference-side
+binding a maintainer would add: the engine class and bench() are swapped, and the drop-in's
+argument errors surface as the reference's own anybcq.UsageError (the
+reference's CLI exit codes and HTTP 400 mapping catch that class,
+cli.py:247-266, service/server.py:107-109).
+"""
+
+import functools
+
+import anybcq
+import anybcq.cli
+import anybcq.errors
+import anybcq.gemv
+import anybcq.service.server
+
+import paper_2510_10467_b200.engine as b200
+from paper_2510_10467_b200.errors import UsageError as B200UsageError
+
+
+def _ref_errors(fn):
+    @functools.wraps(fn)
+    def wrapped(*a, **k):
+        try:
+            return fn(*a, **k)
+        except B200UsageError as exc:
+            raise anybcq.errors.UsageError(str(exc)) from exc
+    return wrapped
+
+
+class GemvEngine(b200.GemvEngine):
+    __init__ = _ref_errors(b200.GemvEngine.__init__)
+    lut = _ref_errors(b200.GemvEngine.lut)
+    naive = _ref_errors(b200.GemvEngine.naive)
+
+
+def gemv_lut(model, p, x, chunk_width=8):
+    return GemvEngine(model, chunk_width).lut(p, x)
+
+
+def gemv_naive(model, p, x):
+    return GemvEngine(model).naive(p, x)
+
+
+bench = _ref_errors(b200.bench)   # device-timed (CUDA events), same rows and counters
+
+for _mod in (anybcq, anybcq.gemv, anybcq.cli, anybcq.service.server):
+    _mod.GemvEngine = GemvEngine
+    _mod.bench = bench
+for _mod in (anybcq, anybcq.gemv):
+    _mod.gemv_lut = gemv_lut
+    _mod.gemv_naive = gemv_naive

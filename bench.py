@@ -1,33 +1,44 @@
 #!/usr/bin/env python
-"""Benchmark: AnyBCQ bit-plane GEMV on B200 (BASELINE.json configs[1]).
+"""Benchmark: AnyBCQ bit-plane GEMV on B200 (BASELINE.json configs[1] headline,
+every other BASELINE config reported beside it).
 
-One *step* = the Llama-3-8B layer-shape sweep (q, k, v, o, gate, up, down)
-GEMV at batch 1 for every precision p in {2, 3, 4} (21 GEMVs), on synthetic
-packed planes (splitmix64 words) and fp16 scales, x in fp16, y in fp16.
+Headline step = the Llama-3-8B layer-shape sweep (q, k, v, o, gate, up, down)
+GEMV at batch 1 for every precision p in {2, 3, 4} (21 GEMVs = 21 requests
+with per-request precision) on synthetic packed planes (splitmix64 words,
+tensor_io.random_words) and fp16 scales, x and y in fp16, run as ONE
+persistent mixed-precision batched launch (+ its split-K reduce launch).
 
-  value  = algorithmic bytes of the step / device time  [GB/s]
-           (bytes = p-plane bytes + scale-set-p bytes + x + y)
-  e2e    = the same through the public API with pinned HOST x/y
-           (H2D of x + D2H of y per GEMV inside the timed region)
-  roofline: the LUT kernel is the only kernel in the step; achieved =
-           algorithmic bytes / kernel time, peak = MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline: the reference's LUT algorithm restated in C (oracle/),
-           all host threads, on a bounded sample of the same workload
+  value    = algorithmic bytes of the step / device time  [GB/s]
+             (bytes = p-plane bytes + scale-set-p bytes + x + y)
+  parity   = one untimed step of the EXACT timed configuration checked against
+             the C port of GemvEngine.lut on the identical host inputs
+  e2e      = the same through the public API with pinned HOST x/y
+  roofline = the LUT kernel (the only kernel of the step); achieved =
+             algorithmic bytes / kernel time, peak = MEASURED_PEAKS.json
+  cpu_baseline: the reference's LUT algorithm restated in C (oracle/), all
+             host threads and one thread, plus the real reference (numba,
+             baseline/_ref) on a 4096x4096 layer when installed
+  config1..config5: BASELINE.json configs[0..4] (see each key's "what")
 
 L2: three copies of the layer set (one per precision) so that every plane
-byte is re-read only after a full step (>= 245 MB > 126 MB L2).
+byte is re-read only after a full step (>= 245 MB > 126 MB L2); per-shape
+pools rotate over copies whose total exceeds 2x L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-For N > 1 (torchrun): each rank holds a 1/N row shard of layers N x taller
-(per-rank work = the 1-GPU step, weak scaling) and every GEMV output is
-all-gathered over NCCL.
+For N > 1 (torchrun; `--gpus N` without torchrun re-launches itself under
+torchrun): each rank holds a 1/N row shard of layers N x taller (per-rank
+work = the 1-GPU step, weak scaling) and every step's outputs are
+all-gathered over NCCL; config5 row-shards the Llama-3-70B layers over the N
+ranks (strong scaling, GEMV-only and GEMV + all-gather times).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -41,21 +52,21 @@ sys.path.insert(0, str(ROOT))
 
 LAYERS = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
           ("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
-# The timed step runs the 21 independent GEMVs of the sweep (7 layers x
-# p=2,3,4 -- per-request precision, the AnyBCQ serving case) as ONE persistent
-# mixed-precision batched launch (abcq_gemv_batch). Also reported: the same
-# step as one launch per precision, grouped as a decoder issues it
-# ([q,k,v] [o] [gate,up] [down] per p), and as 21 single-GEMV launches.
+LAYERS_70B = [("q", 8192, 8192), ("k", 1024, 8192), ("v", 1024, 8192), ("o", 8192, 8192),
+              ("gate", 28672, 8192), ("up", 28672, 8192), ("down", 8192, 28672)]
 STEP_GROUPS = [tuple(range(7))]
 DECODER_GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
 P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
 XY_BYTES = 2      # fp16 x and y
+L2_BYTES = 126 * 1024 * 1024
 METRIC = "bit-plane GEMV HBM GB/s (Llama-3-8B layer sweep, p=2/3/4, batch 1)"
 WORKLOAD = ("Llama-3-8B layer sweep q/k/v/o/gate/up/down GEMV, batch 1, p=2,3,4 per step, g=128, fp16 "
             "scales/x/y; the 21 independent GEMVs (per-request precision) run as one persistent "
             "mixed-precision batched launch + one split-K reduce launch")
+DTYPE = "f32"   # arithmetic: f32 table entries (reference rounding), f32 group sums and accumulation
+DTYPE_NOTE = "storage: 1-bit sign planes, fp16 scales / x / y; arithmetic f32 (tables, sums, accumulation)"
 
 
 def algo_bytes(rows: int, cols: int, p: int) -> int:
@@ -68,7 +79,25 @@ def step_bytes() -> int:
     return sum(algo_bytes(r, c, p) for p in PRECISIONS for _, r, c in LAYERS)
 
 
-# ---------------------------------------------------------------------------
+def bench_config(world: int) -> dict:
+    """The config dict printed by BOTH arms (identical keys and values)."""
+    return {"workload": WORKLOAD, "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
+            "group_size": 128, "batch": 1, "bytes_per_step": step_bytes(),
+            "l2": f"inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
+                  f"({step_bytes() / 1e6:.0f} MB) > 126 MB",
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def read_peaks():
     try:
         d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -153,69 +182,142 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
 
 
+
+
 # ---------------------------------------------------------------------------
-def make_layer_models(P, row_scale: int, copies: int, seed0: int = 0, p_lo: int = P_LO, p_hi: int = P_HI):
-    """copies x 7 DeviceModels (p p_lo:p_hi, fp16 scales), synthetic planes/scales
-    generated on the host from splitmix64."""
+class Ctx:
+    """What every section needs: torch, the package, the device and stream."""
+
+    def __init__(self, dev, stream, rank, world):
+        import torch
+
+        import paper_2510_10467_b200 as P
+        from paper_2510_10467_b200.device_model import gemv_batch
+
+        self.torch, self.P, self.gemv_batch = torch, P, gemv_batch
+        self.dev, self.stream, self.rank, self.world = dev, stream, rank, world
+
+    def time_graph(self, fn, reps=10):
+        """ms per call of fn: fn captured once as a CUDA graph, replayed reps times."""
+        torch, st = self.torch, self.stream
+        with torch.cuda.stream(st):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
+        with torch.cuda.stream(st):
+            g.replay()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(st)
+            for _ in range(reps):
+                g.replay()
+            a1.record(st)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / reps
+
+    def device_model(self, rows, cols, p_lo, p_hi, seed, asym=False):
+        """A DeviceModel with device-RNG planes and |N|-ish fp16 scales (pools, 70B shards)."""
+        torch = self.torch
+        g = torch.Generator(device=self.dev).manual_seed(seed)
+        dm = self.P.DeviceModel(rows, cols, 128, p_lo, p_hi, asym, scale_dtype="f16", device=self.dev)
+        dm.load_planes(torch.randint(-2**31, 2**31 - 1, (p_hi, rows, cols // 32), dtype=torch.int32,
+                                     device=self.dev, generator=g))
+        for p in range(p_lo, p_hi + 1):
+            a = 0.01 + 0.1 * torch.rand((p, rows, cols // 128), device=self.dev, generator=g)
+            z = 0.1 * torch.randn((rows, cols // 128), device=self.dev, generator=g) if asym else None
+            dm.load_scale_set(p, a, z)
+        return dm
+
+
+def make_layer_models(P, row_scale: int, copies: int, seed0: int = 0, p_lo: int = P_LO, p_hi: int = P_HI,
+                      keep_host: bool = False):
+    """copies x 7 DeviceModels (p p_lo:p_hi, fp16 scales), synthetic planes /
+    scales generated on the host (splitmix64 words); with keep_host
+    the host arrays (words, f16-rounded alphas) are returned for the parity
+    check against the C port on IDENTICAL inputs."""
     from paper_2510_10467_b200.tensor_io import random_words  # (the GPU leg never imports oracle/)
 
-    models = []
+    models, host = [], []
     for c in range(copies):
-        row = []
+        row, hrow = [], []
         for li, (name, r, k) in enumerate(LAYERS):
             rows = r * row_scale
             seed = seed0 + 1000 * c + li
             dm = P.DeviceModel(rows, k, 128, p_lo, p_hi, False, scale_dtype="f16")
-            dm.load_planes(random_words(p_hi, rows, k, seed=seed))
+            words = random_words(p_hi, rows, k, seed=seed)
+            dm.load_planes(words)
             rng = np.random.default_rng(seed)
+            alphas = {}
             for p in range(p_lo, p_hi + 1):
                 a = (0.01 + 0.1 * np.abs(rng.standard_normal((p, rows, k // 128)))).astype(np.float32)
                 dm.load_scale_set(p, a)
+                alphas[p] = a.astype(np.float16).astype(np.float32)  # what the f16 device set holds
             row.append(dm)
+            hrow.append((words, alphas) if keep_host else None)
         models.append(row)
-    return models
+        host.append(hrow)
+    return models, host
+
+
+def parity_check(ctx, models, host, xs_host, ys, jobs):
+    """The exact timed configuration's outputs (already computed by one untimed
+    step) vs the C port of GemvEngine.lut on the identical host inputs."""
+    from oracle import anybcq_oracle as O  # checker only
+    from oracle import c_oracle
+
+    threads = c_oracle.cpu_threads()
+    worst, worst_job, devs = 0.0, None, {}
+    for pi, p, li in jobs:
+        words, alphas = host[pi][li]
+        k = LAYERS[li][2]
+        want = c_oracle.lut_gemv(words, k, 128, alphas[p], None, p, xs_host[k].astype(np.float64), threads)
+        got = ys[pi][li].float().cpu().numpy()
+        d = O.rel_dev(got, want)
+        devs[f"{LAYERS[li][0]}_p{p}"] = float(f"{d:.3e}")
+        if d > worst:
+            worst, worst_job = d, f"{LAYERS[li][0]}_p{p}"
+    return {"max_rel_dev": float(f"{worst:.3e}"), "worst_job": worst_job, "tolerance": 1e-3,
+            "ok": worst <= 1e-3, "per_job": devs,
+            "what": "one untimed step of the exact timed configuration (21 jobs, one batched launch, fp16 x/y/"
+                    "scales) vs the C port of GemvEngine.lut on identical inputs; rel_dev = max|y-y_ref| / "
+                    "max|y_ref| (fp16 y rounding included)"}
 
 
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2510_10467_b200 as P
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    mp = world > 1 or os.environ.get("ABCQ_BENCH_FORCE_MP") == "1"
+    if mp:
         dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Ctx(dev, stream, rank, world)
+    P, gemv_batch = ctx.P, ctx.gemv_batch
 
     copies = len(PRECISIONS)
-    models = make_layer_models(P, 1, copies, seed0=17 * rank)
-    xs = {k: (torch.randn(k, device=dev) * 1.0).half() for k in {c for _, _, c in LAYERS}}
+    models, host = make_layer_models(P, 1, copies, seed0=17 * rank, keep_host=(rank == 0))
+    rng = np.random.default_rng(1234 + rank)
+    xs_host = {k: rng.standard_normal(k).astype(np.float16) for k in sorted({c for _, _, c in LAYERS})}
+    xs = {k: torch.from_numpy(v).to(dev) for k, v in xs_host.items()}
     ys = [[torch.empty(m.rows, dtype=torch.float16, device=dev) for m in row] for row in models]
-    # multi-GPU step: the 21 row-sharded outputs of a step live in ONE flat
-    # buffer, all-gathered by ONE NCCL call that overlaps the next step's
-    # GEMV launch (two buffer sets; a step waits only for the gather that last
-    # read its buffer)
-    mp = world > 1 or os.environ.get("ABCQ_BENCH_FORCE_MP") == "1"
-    if mp and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev)
-
-    stream = torch.cuda.Stream(device=dev)
-
-    from paper_2510_10467_b200.device_model import gemv_batch
-
-    def grouped_launches(groups):  # (rank 0 only: local launches, no collectives)
-        for pi, p in enumerate(PRECISIONS):
-            for grp in groups:
-                gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], stream)
-
     all_jobs = [(pi, p, li) for pi, p in enumerate(PRECISIONS) for li in range(len(LAYERS))]
 
-    def step_launches():  # single GPU (multi-GPU: step_mp)
+    def step_launches():
         gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for pi, p, li in all_jobs], stream)
 
+    # multi-GPU step: the 21 row-sharded outputs of a step live in ONE flat
+    # buffer, all-gathered by ONE NCCL call that overlaps the next step's GEMV
+    # launch (two buffer sets; a step waits only for the gather that last read
+    # its buffer)
     mp_rows = sum(models[pi][li].rows for pi, p, li in all_jobs)
     mp_y = [torch.empty(mp_rows, dtype=torch.float16, device=dev) for _ in range(2)] if mp else None
     mp_g = [torch.empty(mp_rows * world, dtype=torch.float16, device=dev) for _ in range(2)] if mp else None
@@ -234,7 +336,7 @@ def run_gpu(args):
     def step_mp(i):
         b = i & 1
         if mp_work[b] is not None:
-            mp_work[b].wait()  # (stream waits for the gather that last read mp_y[b])
+            mp_work[b].wait()
         mp_plan[b].launch(stream)
         mp_work[b] = dist.all_gather_into_tensor(mp_g[b], mp_y[b], async_op=True)
 
@@ -244,32 +346,14 @@ def run_gpu(args):
                 mp_work[b].wait()
                 mp_work[b] = None
 
-    def single_launches():
-        for pi, p in enumerate(PRECISIONS):
-            for li, m in enumerate(models[pi]):
-                m.gemv(p, xs[m.cols], out=ys[pi][li], stream=stream)
+    # ---- parity of the exact timed configuration (untimed, rank 0) ---------
+    with torch.cuda.stream(stream):
+        step_launches()
+    torch.cuda.synchronize()
+    parity = parity_check(ctx, models, host, xs_host, ys, all_jobs) if rank == 0 else None
+    host = None  # (release the host copies)
 
-    def time_graph(fn, reps=10):
-        with torch.cuda.stream(stream):
-            fn()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            fn()
-        with torch.cuda.stream(stream):
-            g.replay()
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            for _ in range(reps):
-                g.replay()
-            a1.record(stream)
-        torch.cuda.synchronize()
-        return a0.elapsed_time(a1) / reps
-
-    # warm up (allocates per-stream workspaces), then capture the K timed steps
-    # as CUDA graphs of up to 50 consecutive steps each (a graph per step would
-    # leave a replay gap between steps)
+    # warm up, then capture the K timed steps as CUDA graphs of up to 50 steps
     with torch.cuda.stream(stream):
         for i in range(max(args.warmup, 3)):
             step_mp(i) if mp else step_launches()
@@ -277,7 +361,7 @@ def run_gpu(args):
             mp_drain()
     torch.cuda.synchronize()
     use_graph = not mp
-    plan = []  # (graph, steps in it), replayed in order: exactly K steps
+    plan = []
     if use_graph:
         per = min(args.steps, 50)
         sizes = [per] * (args.steps // per) + ([args.steps % per] if args.steps % per else [])
@@ -291,7 +375,7 @@ def run_gpu(args):
                 built[n] = g
             plan.append((built[n], n))
         with torch.cuda.stream(stream):
-            for g in built.values():  # (untimed: first replays)
+            for g in built.values():
                 g.replay()
             for _ in range(args.warmup):
                 step_launches()
@@ -303,7 +387,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        time.sleep(0.02)  # poller running before the region starts
+        time.sleep(0.02)
         clk.mark(True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
@@ -313,7 +397,7 @@ def run_gpu(args):
             else:
                 for i in range(args.steps):
                     step_mp(i)
-                mp_drain()  # the last steps' gathers complete inside the timed region
+                mp_drain()
             ev1.record(stream)
         torch.cuda.synchronize()
         clk.mark(False)
@@ -324,308 +408,596 @@ def run_gpu(args):
         ms = float(t.item())
         dist.barrier()
     ms_step = ms / args.steps
-    total_bytes = step_bytes() * world
-    value = total_bytes / (ms_step * 1e-3) / 1e9
+    value = step_bytes() * world / (ms_step * 1e-3) / 1e9
 
-    # ---- the same step issued as a decoder would, and as 21 single launches --
-    variants = {}
+    peak, peak_kind = read_peaks()
+    sections = set(args.sections.split(",")) if args.sections else None
+    want = (lambda name: sections is None or name in sections)
+
+    # ---- config5: Llama-3-70B layers row-sharded over the N ranks (all ranks)
+    cfg5 = config5_row_sharded(ctx, args, peak) if want("config5") else None
+
+    out = {}
     if rank == 0:
-        for name, fn in (("one_launch_per_precision", lambda: grouped_launches(STEP_GROUPS)),
-                         ("decoder_grouped", lambda: grouped_launches(DECODER_GROUPS)),
-                         ("single_launch_per_gemv", single_launches)):
-            vms = time_graph(fn)
-            variants[name] = {"ms_per_step": round(vms, 4), "GBps": round(step_bytes() / (vms * 1e-3) / 1e9, 1)}
-
-    # ---- per-shape breakdown (device time, back-to-back launches) ----------
-    per_shape = {}
-    if rank == 0:
-        reps = 20
-        for li, (name, r, k) in enumerate(LAYERS):
-            for pi, p in enumerate(PRECISIONS):
-                g2 = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g2, stream=stream):
-                    for j in range(reps):
-                        models[j % copies][li].gemv(p, xs[k], out=ys[j % copies][li], stream=stream)
-                with torch.cuda.stream(stream):   # replay() launches on the current stream
-                    g2.replay()
-                    torch.cuda.synchronize()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    for _ in range(5):
-                        g2.replay()
-                    b.record(stream)
-                torch.cuda.synchronize()
-                us = a.elapsed_time(b) * 1e3 / (5 * reps)
-                per_shape[f"{name}_{r}x{k}_p{p}"] = {
-                    "us": round(us, 3), "GBps": round(algo_bytes(r, k, p) / (us * 1e-6) / 1e9, 1)}
-
-        # ---- p=2 sweep vs the cuBLAS fp16 GEMV sweep, every variant rotating
-        # over weight copies whose total exceeds 2x L2 (5 p=2-only layer sets,
-        # 272 MB; 2 dense fp16 sets, 235 MB), graphs of back-to-back sweeps
-        pool = make_layer_models(P, 1, 5, seed0=500, p_lo=2, p_hi=2)
-        ys2 = [[torch.empty(m.rows, dtype=torch.float16, device=dev) for m in row] for row in pool]
-        dense = [[torch.randn(r, k, device=dev, dtype=torch.float16) * 0.01 for _, r, k in LAYERS] for _ in range(2)]
-        yd = [torch.empty(r, device=dev, dtype=torch.float16) for _, r, _ in LAYERS]
-        fused_w = [{g: torch.cat([d[i] for i in g]) for g in DECODER_GROUPS} for d in dense]
-        fused_y = {g: torch.empty(fused_w[0][g].shape[0], device=dev, dtype=torch.float16) for g in DECODER_GROUPS}
-
-        def per_sweep(fn, n):  # us per sweep: graph of sweeps over copies 0..n-1
-            return 1e3 * time_graph(lambda: [fn(c) for c in range(n)], reps=10) / n
-
-        with torch.cuda.stream(stream):  # cuBLAS handle/workspace before capture
-            torch.mv(dense[0][0], xs[LAYERS[0][2]], out=yd[0])
-        torch.cuda.synchronize()
-        fp16_us = per_sweep(lambda c: [torch.mv(dense[c][li], xs[k], out=yd[li])
-                                       for li, (_, r, k) in enumerate(LAYERS)], 2)
-        fp16g_us = per_sweep(lambda c: [torch.mv(fused_w[c][g], xs[LAYERS[g[0]][2]], out=fused_y[g])
-                                        for g in DECODER_GROUPS], 2)
-        p2_us = per_sweep(lambda c: [m.gemv(2, xs[m.cols], out=ys2[c][li], stream=stream)
-                                     for li, m in enumerate(pool[c])], 5)
-        p2b_us = per_sweep(lambda c: gemv_batch([(m, 2, xs[m.cols], ys2[c][li]) for li, m in enumerate(pool[c])],
-                                                stream), 5)
-        p2g_us = per_sweep(lambda c: [gemv_batch([(pool[c][li], 2, xs[pool[c][li].cols], ys2[c][li]) for li in g],
-                                                 stream) for g in DECODER_GROUPS], 5)
-        # decoder-grouped with q/k/v and gate/up as row-stacked AnyBCQ models (one
-        # GEMV per group, as the decode harness runs them; cuBLAS likewise on
-        # the concatenated fp16 weights) -- BCQ is per row and group: exact
-        from paper_2510_10467_b200.tensor_io import random_words
-        stacked = []
-        for c in range(5):
-            row = []
-            for gi, g in enumerate(DECODER_GROUPS):
-                r, k = sum(LAYERS[i][1] for i in g), LAYERS[g[0]][2]
-                dm = P.DeviceModel(r, k, 128, 2, 2, False, scale_dtype="f16")
-                dm.load_planes(random_words(2, r, k, seed=900 + 10 * c + gi))
-                dm.load_scale_set(2, (0.01 + 0.1 * np.abs(np.random.default_rng(c).standard_normal(
-                    (2, r, k // 128)))).astype(np.float32))
-                row.append(dm)
-            stacked.append(row)
-        ys_st = [torch.empty(m.rows, dtype=torch.float16, device=dev) for m in stacked[0]]
-        p2s_us = per_sweep(lambda c: [m.gemv(2, xs[m.cols], out=ys_st[gi], stream=stream)
-                                      for gi, m in enumerate(stacked[c])], 5)
-        del stacked
-        fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)
-        fp16 = {"us_per_sweep": round(fp16_us, 2), "GBps": round(fp16_bytes / (fp16_us * 1e-6) / 1e9, 1),
-                "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2),
-                "abcq_p2_batched_us_per_sweep": round(p2b_us, 2), "speedup_p2_batched": round(fp16_us / p2b_us, 2),
-                "decoder_grouped": {"cublas_fp16_us": round(fp16g_us, 2), "abcq_p2_us": round(p2g_us, 2),
-                                    "speedup_p2": round(fp16g_us / p2g_us, 2),
-                                    "abcq_p2_stacked_us": round(p2s_us, 2),
-                                    "speedup_p2_stacked": round(fp16g_us / p2s_us, 2),
-                                    "stacked": "q/k/v and gate/up as one row-stacked AnyBCQ model each "
-                                               "(4 single GEMVs per sweep, as tools/decode_bench.py runs them)",
-                                    "launches": "4 per sweep each: [q,k,v] [o] [gate,up] [down] (cuBLAS on "
-                                                "concatenated fp16 weights)"},
-                "note": "7 layers at p=2 vs fp16: cuBLAS 7 torch.mv; abcq 7 single launches / 1 gemv_batch / "
-                        "4 decoder-grouped gemv_batch; weights rotate over copies > 2x L2"}
-        del pool, fused_w
-        del dense
-
-    # ---- per shape, launch latency amortised: one gemv_batch of 8 independent
-    # same-shape GEMVs (8 distinct weight sets, e.g. 8 adapters / requests on
-    # different models), back to back over 2 such groups (> 2x L2 for the big
-    # shapes; the small ones are partly L2-resident -- reported as measured)
-    per_shape_b8 = {}
-    if rank == 0 and not args.no_cpu:
-        peak8, _ = read_peaks()
-        for li, (name, r, k) in enumerate(LAYERS):
-            if name in ("k", "v", "o", "up"):  # same shapes as q / gate
-                continue
-            pool8 = []
-            for c in range(16):
-                dm = P.DeviceModel(r, k, 128, P_LO, P_HI, False, scale_dtype="f16")
-                dm.load_planes(torch.randint(-2**31, 2**31 - 1, (P_HI, r, k // 32), dtype=torch.int32, device=dev))
-                for pp in PRECISIONS:
-                    dm.load_scale_set(pp, 0.01 + 0.1 * torch.rand(pp, r, k // 128, device=dev))
-                pool8.append(dm)
-            yb = [torch.empty(r, dtype=torch.float16, device=dev) for _ in range(16)]
-            for pp in PRECISIONS:
-                us = 1e3 * time_graph(lambda: [gemv_batch([(pool8[8 * h + j], pp, xs[k], yb[8 * h + j]) for j in range(8)],
-                                                          stream) for h in range(2)], reps=10) / 2
-                gbps = 8 * algo_bytes(r, k, pp) / (us * 1e-6) / 1e9
-                per_shape_b8[f"{name}_{r}x{k}_p{pp}"] = {"us_per_launch": round(us, 2), "GBps": round(gbps, 1),
-                                                         "roofline_frac": round(gbps / peak8, 4)}
-            del pool8, yb
-
-    # ---- e2e: public API with pinned host buffers, copies in the timed region
-    e2e = None
-    if rank == 0:
-        # one pinned staging buffer each way per step: x of both input widths
-        # in, the 21 outputs out (views of one device buffer) -- one copy per
-        # direction and step. Serving-style pipeline: two buffer sets, the H2D
-        # of step i+1 and the D2H of step i on their own streams overlap the
-        # GEMV launch of step i (event-ordered; every step still moves its
-        # own bytes both ways inside the timed region)
-        kx = sorted(xs)
-        hx = torch.cat([xs[k].cpu() for k in kx]).pin_memory()
-        n_out = sum(models[pi][li].rows for pi, p, li in all_jobs)
-        sets = []
-        for _ in range(2):
-            dxa = torch.empty_like(hx, device=dev)
-            dx, off = {}, 0
-            for k in kx:
-                dx[k] = dxa[off:off + k]
-                off += k
-            dya = torch.empty(n_out, dtype=torch.float16, device=dev)
-            dys, off = [], 0
-            for pi, p, li in all_jobs:
-                dys.append(dya[off:off + models[pi][li].rows])
-                off += models[pi][li].rows
-            sets.append({"dxa": dxa, "dx": dx, "dya": dya, "dys": dys,
-                         "hy": torch.empty(n_out, dtype=torch.float16).pin_memory(),
-                         "in": torch.cuda.Event(), "comp": torch.cuda.Event(), "out": torch.cuda.Event()})
-        for S in sets:  # the public API's repeated-launch form (validated and marshalled once)
-            S["plan"] = P.GemvBatchPlan([(models[pi][li], p, S["dx"][models[pi][li].cols], S["dys"][n])
-                                         for n, (pi, p, li) in enumerate(all_jobs)])
-        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        h2d = d2h = 0
-
-        def e2e_step(i):
-            nonlocal h2d, d2h
-            S = sets[i & 1]
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(S["comp"])  # the GEMV that last read this x buffer is done
-                S["dxa"].copy_(hx, non_blocking=True)
-                S["in"].record(s_in)
-            h2d += hx.numel() * 2
-            stream.wait_event(S["in"])
-            stream.wait_event(S["out"])  # the D2H that last read this y buffer is done
-            S["plan"].launch(stream)
-            S["comp"].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(S["comp"])
-                S["hy"].copy_(S["dya"], non_blocking=True)
-                S["out"].record(s_out)
-            d2h += S["dya"].numel() * 2
-
-        with torch.cuda.stream(stream):
-            for S in sets:
-                for e in ("in", "comp", "out"):
-                    S[e].record(stream)
-            for i in range(4):
-                e2e_step(i)
-            torch.cuda.synchronize()
-            h2d = d2h = 0
-            n_e2e = max(4, min(args.steps, 50))
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            s_in.wait_stream(stream)
-            s_out.wait_stream(stream)
-            for i in range(n_e2e):
-                e2e_step(i)
-            stream.wait_stream(s_out)
-            b.record(stream)
-            torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(b) / n_e2e
-        e2e = {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
-               "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d // n_e2e,
-               "d2h_bytes_per_step": d2h // n_e2e,
-               "api": "GemvBatchPlan.launch of the 21 GEMVs (one C-ABI abcq_gemv_batch call per step), eager; "
-                      "pinned host x in and y out, one copy each way per step, copies of neighbouring steps "
-                      "overlapped on two side streams"}
+        if want("variants"):
+            out.update(step_variants(ctx, models, xs, ys, peak))
+        if want("per_shape"):
+            out["per_shape"] = per_shape(ctx, xs)
+        if want("fp16"):
+            out["fp16_cublas"] = fp16_comparison(ctx, xs)
+        if want("batched8"):
+            out["per_shape_batched8"] = per_shape_batched8(ctx, xs, peak)
+        if want("e2e"):
+            out["e2e"] = e2e_section(ctx, models, xs, all_jobs, args)
+        if want("config1"):
+            out["config1"] = config1(ctx, args, peak)
+        if want("config3"):
+            out["config3"] = config3(ctx)
+        if want("config4"):
+            out["config4"] = config4(ctx, args)
+    if mp:
+        dist.barrier()
 
     if rank == 0:
-        peak, peak_kind = read_peaks()
-        kernel_bytes = step_bytes()
-        achieved = kernel_bytes / (ms_step * 1e-3) / 1e9
+        achieved = step_bytes() / (ms_step * 1e-3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "ncu_traffic.json"
-        if tf.exists():  # ncu dram__bytes_read+write per launch of the batched kernel (profiles/)
+        if tf.exists():
             try:
                 traffic = int(json.loads(tf.read_text())["traffic_bytes_per_launch"])
             except Exception:
                 traffic = None
         cpu = cpu_baseline() if world == 1 and not args.no_cpu else None
+        config = bench_config(world)
+        config["timing"] = ("the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream"
+                            if not mp else "eager steps, one NCCL all-gather of the step's 21 outputs per step "
+                            "overlapping the next step (double-buffered), CUDA events, max over ranks")
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+            "dtype_note": DTYPE_NOTE,
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
-            "config": {"workload": WORKLOAD,
-                       "layers": {n: [r, k] for n, r, k in LAYERS}, "precisions": list(PRECISIONS),
-                       "bytes_per_step": kernel_bytes,
-                       "l2": "inputs larger than L2: 3 plane-set copies, reuse distance = 1 step "
-                             f"({kernel_bytes / 1e6:.0f} MB) > 126 MB",
-                       "timing": ("the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream"
-                                  if not mp else "eager steps, one NCCL all-gather of the step's 21 outputs per "
-                                  "step overlapping the next step (double-buffered), CUDA events, max over ranks"),
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU"},
+            "config": config,
             # per step: the persistent batched GEMV kernel + the split-K reduce kernel
-            "gpu_launches": args.steps * 2,  # (+ one NCCL all-gather per step when multi-GPU)
-            "step_variants": variants,
-            "e2e": e2e,
+            "gpu_launches": args.steps * 2,
+            "parity": parity,
+            "e2e": out.pop("e2e", None),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                          "kernel": "abcq::gemv_batch_kernel (+ batch_reduce_kernel)", "traffic": traffic,
-                         "algorithmic_bytes_per_step": kernel_bytes},
+                         "algorithmic_bytes_per_step": step_bytes()},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "per_shape": per_shape,
-            "per_shape_batched8": per_shape_b8,
-            "per_shape_batched8_note": "one gemv_batch of 8 independent same-shape GEMVs (distinct weights) per "
-                                       "launch, back to back: the per-shape kernel rate with the launch latency "
-                                       "amortised",
-            "per_shape_note": "single launches, graph of 20 back-to-back launches rotating 3 weight copies "
-                              "(the smaller layers can be partly L2-resident)",
-            "fp16_cublas": fp16,
+            "config5": cfg5,
         }
+        line.update(out)
         print(json.dumps(line))
     if mp:
         dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
-def _cpu_sample_models():
-    from oracle import anybcq_oracle as O
-    out = []
+def step_variants(ctx, models, xs, ys, peak):
+    """The same 21 GEMVs issued as a decoder would (one batched launch per
+    [q,k,v] [o] [gate,up] [down] group and precision), as 21 single launches,
+    and one launch per precision; each with its roofline fraction."""
+    gemv_batch, st = ctx.gemv_batch, ctx.stream
+
+    def grouped(groups):
+        for pi, p in enumerate(PRECISIONS):
+            for grp in groups:
+                gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], st)
+
+    def singles():
+        for pi, p in enumerate(PRECISIONS):
+            for li, m in enumerate(models[pi]):
+                m.gemv(p, xs[m.cols], out=ys[pi][li], stream=st)
+
+    res = {}
+    for name, fn in (("one_launch_per_precision", lambda: grouped(STEP_GROUPS)),
+                     ("decoder_grouped", lambda: grouped(DECODER_GROUPS)),
+                     ("single_launch_per_gemv", singles)):
+        ms = ctx.time_graph(fn)
+        gbps = step_bytes() / (ms * 1e-3) / 1e9
+        res[name] = {"ms_per_step": round(ms, 4), "GBps": round(gbps, 1), "roofline_frac": round(gbps / peak, 4)}
+    return {"step_variants": res,
+            "roofline_decoder_grouped": {"bound": "hbm", "achieved": res["decoder_grouped"]["GBps"], "peak": peak,
+                                         "unit": "GB/s", "frac": res["decoder_grouped"]["roofline_frac"],
+                                         "what": "the step's 21 GEMVs as a decoder issues them: 4 launches per "
+                                                 "precision ([q,k,v] [o] [gate,up] [down], each a batched launch)"},
+            "roofline_single_launch": {"bound": "hbm", "achieved": res["single_launch_per_gemv"]["GBps"],
+                                       "peak": peak, "unit": "GB/s",
+                                       "frac": res["single_launch_per_gemv"]["roofline_frac"],
+                                       "what": "21 dependent-style single-GEMV launches back to back"}}
+
+
+def _pool(ctx, rows, cols, p_lo, p_hi, seed0, min_copies=2, max_copies=64):
+    """Copies of one shape whose plane bytes exceed 2x L2 (capped)."""
+    per = p_hi * rows * cols // 8
+    n = max(min_copies, min(max_copies, math.ceil(2 * L2_BYTES / per) + 1))
+    return [ctx.device_model(rows, cols, p_lo, p_hi, seed0 + c) for c in range(n)]
+
+
+def per_shape(ctx, xs):
+    """Single launches back to back (graph of 20), rotating over > 2x L2 of copies."""
+    torch = ctx.torch
+    res = {}
     for li, (name, r, k) in enumerate(LAYERS):
-        words = O.random_words(P_HI, r, k, seed=li)
-        rng = np.random.default_rng(li)
-        alphas = {p: (0.01 + 0.1 * np.abs(rng.standard_normal((p, r, k // 128)))).astype(np.float16)
-                  .astype(np.float32) for p in PRECISIONS}
-        out.append((name, r, k, words, alphas))
+        if name in ("v", "up"):  # same shapes as k / gate
+            continue
+        pool = _pool(ctx, r, k, P_LO, P_HI, 7000 + 100 * li)
+        y = torch.empty(r, dtype=torch.float16, device=ctx.dev)
+        for p in PRECISIONS:
+            n = 20
+            ms = ctx.time_graph(lambda: [pool[j % len(pool)].gemv(p, xs[k], out=y, stream=ctx.stream)
+                                         for j in range(n)], reps=5)
+            us = ms * 1e3 / n
+            res[f"{name}_{r}x{k}_p{p}"] = {"us": round(us, 3), "GBps": round(algo_bytes(r, k, p) / (us * 1e-6) / 1e9, 1),
+                                           "copies": len(pool)}
+        del pool
+    res["note"] = ("single GEMV launches back to back (graph of 20), rotating over weight copies totalling > 2x L2 "
+                   "(capped at 64 copies); the small layers are latency-bound")
+    return res
+
+
+def fp16_comparison(ctx, xs):
+    """p=2 sweep vs the cuBLAS fp16 GEMV sweep, rotating over > 2x L2."""
+    torch, P, gemv_batch, st, dev = ctx.torch, ctx.P, ctx.gemv_batch, ctx.stream, ctx.dev
+    pool, _ = make_layer_models(P, 1, 5, seed0=500, p_lo=2, p_hi=2)
+    ys2 = [[torch.empty(m.rows, dtype=torch.float16, device=dev) for m in row] for row in pool]
+    dense = [[torch.randn(r, k, device=dev, dtype=torch.float16) * 0.01 for _, r, k in LAYERS] for _ in range(2)]
+    yd = [torch.empty(r, device=dev, dtype=torch.float16) for _, r, _ in LAYERS]
+    fused_w = [{g: torch.cat([d[i] for i in g]) for g in DECODER_GROUPS} for d in dense]
+    fused_y = {g: torch.empty(fused_w[0][g].shape[0], device=dev, dtype=torch.float16) for g in DECODER_GROUPS}
+
+    def per_sweep(fn, n):
+        return 1e3 * ctx.time_graph(lambda: [fn(c) for c in range(n)], reps=10) / n
+
+    with torch.cuda.stream(st):
+        torch.mv(dense[0][0], xs[LAYERS[0][2]], out=yd[0])
+    torch.cuda.synchronize()
+    fp16_us = per_sweep(lambda c: [torch.mv(dense[c][li], xs[k], out=yd[li]) for li, (_, r, k) in enumerate(LAYERS)], 2)
+    fp16g_us = per_sweep(lambda c: [torch.mv(fused_w[c][g], xs[LAYERS[g[0]][2]], out=fused_y[g])
+                                    for g in DECODER_GROUPS], 2)
+    p2_us = per_sweep(lambda c: [m.gemv(2, xs[m.cols], out=ys2[c][li], stream=st) for li, m in enumerate(pool[c])], 5)
+    p2b_us = per_sweep(lambda c: gemv_batch([(m, 2, xs[m.cols], ys2[c][li]) for li, m in enumerate(pool[c])], st), 5)
+    p2g_us = per_sweep(lambda c: [gemv_batch([(pool[c][li], 2, xs[pool[c][li].cols], ys2[c][li]) for li in g], st)
+                                  for g in DECODER_GROUPS], 5)
+    stacked = []
+    for c in range(5):
+        stacked.append([ctx.device_model(sum(LAYERS[i][1] for i in g), LAYERS[g[0]][2], 2, 2, 900 + 10 * c + gi)
+                        for gi, g in enumerate(DECODER_GROUPS)])
+    ys_st = [torch.empty(m.rows, dtype=torch.float16, device=dev) for m in stacked[0]]
+    p2s_us = per_sweep(lambda c: [m.gemv(2, xs[m.cols], out=ys_st[gi], stream=st) for gi, m in enumerate(stacked[c])], 5)
+    fp16_bytes = sum(r * k * 2 + k * 2 + r * 2 for _, r, k in LAYERS)
+    return {"us_per_sweep": round(fp16_us, 2), "GBps": round(fp16_bytes / (fp16_us * 1e-6) / 1e9, 1),
+            "abcq_p2_us_per_sweep": round(p2_us, 2), "speedup_p2": round(fp16_us / p2_us, 2),
+            "abcq_p2_batched_us_per_sweep": round(p2b_us, 2), "speedup_p2_batched": round(fp16_us / p2b_us, 2),
+            "decoder_grouped": {"cublas_fp16_us": round(fp16g_us, 2), "abcq_p2_us": round(p2g_us, 2),
+                                "speedup_p2": round(fp16g_us / p2g_us, 2),
+                                "abcq_p2_stacked_us": round(p2s_us, 2),
+                                "speedup_p2_stacked": round(fp16g_us / p2s_us, 2),
+                                "stacked": "q/k/v and gate/up as one row-stacked AnyBCQ model each (4 single "
+                                           "GEMVs per sweep, as the decode harness runs them)",
+                                "launches": "4 per sweep each: [q,k,v] [o] [gate,up] [down] (cuBLAS on "
+                                            "concatenated fp16 weights)"},
+            "note": "7 layers at p=2 vs fp16: cuBLAS 7 torch.mv vs abcq 7 single launches (like for like); "
+                    "1 gemv_batch; 4 decoder-grouped launches; weights rotate over copies > 2x L2"}
+
+
+def per_shape_batched8(ctx, xs, peak):
+    """One gemv_batch of 8 independent same-shape GEMVs per launch: the
+    per-shape kernel rate with the launch latency amortised."""
+    torch, gemv_batch = ctx.torch, ctx.gemv_batch
+    res = {}
+    for li, (name, r, k) in enumerate(LAYERS):
+        if name in ("k", "v", "o", "up"):
+            continue
+        pool8 = [ctx.device_model(r, k, P_LO, P_HI, 3000 + 50 * li + c) for c in range(16)]
+        yb = [torch.empty(r, dtype=torch.float16, device=ctx.dev) for _ in range(16)]
+        for pp in PRECISIONS:
+            us = 1e3 * ctx.time_graph(lambda: [gemv_batch([(pool8[8 * h + j], pp, xs[k], yb[8 * h + j])
+                                                           for j in range(8)], ctx.stream) for h in range(2)],
+                                      reps=10) / 2
+            gbps = 8 * algo_bytes(r, k, pp) / (us * 1e-6) / 1e9
+            res[f"{name}_{r}x{k}_p{pp}"] = {"us_per_launch": round(us, 2), "GBps": round(gbps, 1),
+                                            "roofline_frac": round(gbps / peak, 4)}
+        del pool8, yb
+    return res
+
+
+def e2e_section(ctx, models, xs, all_jobs, args):
+    """Public API with pinned host buffers, copies inside the timed region."""
+    torch, P, st, dev = ctx.torch, ctx.P, ctx.stream, ctx.dev
+    kx = sorted(xs)
+    hx = torch.cat([xs[k].cpu() for k in kx]).pin_memory()
+    n_out = sum(models[pi][li].rows for pi, p, li in all_jobs)
+    sets = []
+    for _ in range(2):
+        dxa = torch.empty_like(hx, device=dev)
+        dx, off = {}, 0
+        for k in kx:
+            dx[k] = dxa[off:off + k]
+            off += k
+        dya = torch.empty(n_out, dtype=torch.float16, device=dev)
+        dys, off = [], 0
+        for pi, p, li in all_jobs:
+            dys.append(dya[off:off + models[pi][li].rows])
+            off += models[pi][li].rows
+        sets.append({"dxa": dxa, "dx": dx, "dya": dya, "dys": dys,
+                     "hy": torch.empty(n_out, dtype=torch.float16).pin_memory(),
+                     "in": torch.cuda.Event(), "comp": torch.cuda.Event(), "out": torch.cuda.Event()})
+    for S in sets:
+        S["plan"] = P.GemvBatchPlan([(models[pi][li], p, S["dx"][models[pi][li].cols], S["dys"][n])
+                                     for n, (pi, p, li) in enumerate(all_jobs)])
+    s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    cnt = {"h2d": 0, "d2h": 0}
+
+    def e2e_step(i):
+        S = sets[i & 1]
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(S["comp"])
+            S["dxa"].copy_(hx, non_blocking=True)
+            S["in"].record(s_in)
+        cnt["h2d"] += hx.numel() * 2
+        st.wait_event(S["in"])
+        st.wait_event(S["out"])
+        S["plan"].launch(st)
+        S["comp"].record(st)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(S["comp"])
+            S["hy"].copy_(S["dya"], non_blocking=True)
+            S["out"].record(s_out)
+        cnt["d2h"] += S["dya"].numel() * 2
+
+    with torch.cuda.stream(st):
+        for S in sets:
+            for e in ("in", "comp", "out"):
+                S[e].record(st)
+        for i in range(4):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        cnt["h2d"] = cnt["d2h"] = 0
+        n_e2e = max(4, min(args.steps, 50))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        s_in.wait_stream(st)
+        s_out.wait_stream(st)
+        for i in range(n_e2e):
+            e2e_step(i)
+        st.wait_stream(s_out)
+        b.record(st)
+        torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / n_e2e
+    return {"value": round(step_bytes() / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+            "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": cnt["h2d"] // n_e2e,
+            "d2h_bytes_per_step": cnt["d2h"] // n_e2e,
+            "api": "GemvBatchPlan.launch of the 21 GEMVs (one C-ABI abcq_gemv_batch call per step), eager; "
+                   "pinned host x in and y out, one copy each way per step, copies of neighbouring steps "
+                   "overlapped on two side streams"}
+
+
+def config1(ctx, args, peak):
+    """BASELINE configs[0]: one 4096x4096 BCQ linear, g=128, batch 1, p=2/3/4 --
+    device time (single launches back to back over > 2x L2 of copies), the
+    drop-in GemvEngine.lut with host numpy in/out (the reference's API), the
+    cuBLAS fp16 GEMV, and the reference's CPU path beside it."""
+    torch = ctx.torch
+    r = k = 4096
+    pool = _pool(ctx, r, k, P_LO, P_HI, 11000)
+    x = torch.randn(k, device=ctx.dev).half()
+    y = torch.empty(r, dtype=torch.float16, device=ctx.dev)
+    res = {"shape": [r, k], "copies": len(pool)}
+    for p in PRECISIONS:
+        n = 20
+        ms = ctx.time_graph(lambda: [pool[j % len(pool)].gemv(p, x, out=y, stream=ctx.stream) for j in range(n)],
+                            reps=10)
+        us = ms * 1e3 / n
+        gbps = algo_bytes(r, k, p) / (us * 1e-6) / 1e9
+        res[f"p{p}"] = {"us": round(us, 3), "GBps": round(gbps, 1), "roofline_frac": round(gbps / peak, 4)}
+    dense = [torch.randn(r, k, device=ctx.dev, dtype=torch.float16) * 0.01 for _ in range(8)]
+    with torch.cuda.stream(ctx.stream):
+        torch.mv(dense[0], x, out=y)
+    torch.cuda.synchronize()
+    ms = ctx.time_graph(lambda: [torch.mv(dense[j % 8], x, out=y) for j in range(16)], reps=10)
+    res["cublas_fp16_us"] = round(ms * 1e3 / 16, 3)
+    res["speedup_vs_fp16"] = {f"p{p}": round(res["cublas_fp16_us"] / res[f"p{p}"]["us"], 2) for p in PRECISIONS}
+    # the drop-in (reference API): numpy in, (f64[N], GemvStats) out, a sync per call
+    from paper_2510_10467_b200.engine import GemvEngine
+    eng = GemvEngine(pool[0])
+    xh = np.random.default_rng(3).standard_normal(k).astype(np.float32)
+    for p in PRECISIONS:
+        for _ in range(3):
+            eng.lut(p, xh)
+        t0 = time.perf_counter()
+        n = 50
+        for _ in range(n):
+            eng.lut(p, xh)
+        res[f"p{p}"]["dropin_lut_us"] = round((time.perf_counter() - t0) / n * 1e6, 1)
+    del pool, dense
+    if not args.no_cpu:
+        res["cpu"] = cpu_layer_times(r, k)
+    res["what"] = ("BASELINE configs[0]: single BCQ linear 4096x4096, group 128, batch 1; us = device time per "
+                   "GEMV back to back; dropin_lut_us = GemvEngine.lut(p, numpy x) end to end (H2D, launch, D2H, "
+                   "f64 cast, host timer); cpu = the reference's LUT path on this host")
+    return res
+
+
+def cpu_layer_times(rows, cols):
+    """The reference's CPU path on one rows x cols layer, p=2/3/4: the C port
+    (1 thread and all threads) and, when baseline/_ref holds the real
+    reference, its numba GemvEngine.lut with the reference's own _time_calls
+    (median of 32 after one warm-up, gemv.py:296-305) at ANYBCQ_THREADS=1/0."""
+    from oracle import anybcq_oracle as O  # checker / baseline only
+    from oracle import c_oracle
+
+    words = O.random_words(P_HI, rows, cols, seed=5)
+    rng = np.random.default_rng(5)
+    alphas = {p: (0.01 + 0.1 * np.abs(rng.standard_normal((p, rows, cols // 128)))).astype(np.float32)
+              for p in PRECISIONS}
+    x = rng.standard_normal(cols)
+    out = {"cpu_model": cpu_model(), "host_threads": c_oracle.cpu_threads()}
+    for th in (1, c_oracle.cpu_threads()):
+        row = {}
+        for p in PRECISIONS:
+            c_oracle.lut_gemv(words, cols, 128, alphas[p], None, p, x, th)
+            reps = 5 if th == 1 else 20
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                c_oracle.lut_gemv(words, cols, 128, alphas[p], None, p, x, th)
+            row[f"p{p}_us"] = round((time.perf_counter() - t0) / reps * 1e6, 1)
+        out[f"c_port_{th}_threads"] = row
+    ref = numba_reference_times(words, alphas, rows, cols, x)
+    if ref is not None:
+        out["reference_numba"] = ref
     return out
 
 
+def numba_reference_times(words, alphas, rows, cols, x):
+    """The unmodified reference (baseline/_ref) GemvEngine.lut, timed by its own
+    _time_calls, in a subprocess per thread setting (ANYBCQ_THREADS)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "anybcq").exists():
+        return None
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        np.savez(Path(td) / "m.npz", words=words, x=x, **{f"a{p}": a for p, a in alphas.items()})
+        code = (
+            "import json,sys,numpy as np\n"
+            "from anybcq import MultiPrecisionModel, QuantConfig, GemvEngine\n"
+            "from anybcq.packing import BitPlaneSet\n"
+            "from anybcq.bcq import ScaleTensor\n"
+            "from anybcq.gemv import _time_calls\n"
+            f"z=np.load(sys.argv[1]); rows,cols={rows},{cols}\n"
+            f"sets={{p: ScaleTensor(z['a%d'%p], None, 128) for p in {list(PRECISIONS)}}}\n"
+            f"m=MultiPrecisionModel(BitPlaneSet({P_HI}, rows, cols, z['words']), sets, {P_LO}, {P_HI}, QuantConfig(128))\n"
+            "e=GemvEngine(m); x=z['x']; out={}\n"
+            f"for p in {list(PRECISIONS)}:\n"
+            "    med, lo = _time_calls(lambda: e.lut(p, x), 32)\n"
+            "    out['p%d_us' % p] = round(med, 1)\n"
+            "print(json.dumps(out))\n")
+        res = {}
+        for th in ("1", "0"):
+            env = dict(os.environ, PYTHONPATH=str(ref), ANYBCQ_THREADS=th, NUMBA_CACHE_DIR=str(Path(td) / "nb"))
+            try:
+                r = subprocess.run([sys.executable, "-c", code, str(Path(td) / "m.npz")], env=env,
+                                   capture_output=True, text=True, timeout=600)
+                res["threads_" + ("1" if th == "1" else "all")] = json.loads(r.stdout.strip().splitlines()[-1])
+            except Exception as exc:  # noqa: BLE001
+                res["threads_" + th] = f"failed: {str(exc)[:100]}"
+        res["what"] = ("unmodified reference anybcq.GemvEngine.lut (numba) from baseline/_ref, its own "
+                       "_time_calls: median us of 32 calls after one warm-up; ANYBCQ_THREADS=1 and 0 (all)")
+        return res
+
+
+def config3(ctx):
+    """BASELINE configs[2]: batch B = 1..16 requests with mixed per-request p on
+    a Llama-3-8B MLP block (gate, up: 14336x4096; down: 4096x14336): the
+    mixed-precision GEMM (one pass over planes 0..max p) vs the B requests as
+    B LUT GEMVs in one batched launch, per matrix; 3 block copies (> 2x L2)."""
+    torch, gemv_batch, st = ctx.torch, ctx.gemv_batch, ctx.stream
+    shapes = [("gate", 14336, 4096), ("up", 14336, 4096), ("down", 4096, 14336)]
+    blocks = [[ctx.device_model(r, k, P_LO, P_HI, 21000 + 10 * c + i) for i, (_, r, k) in enumerate(shapes)]
+              for c in range(3)]
+    res = {}
+    for B in (1, 2, 4, 8, 16):
+        ps = [2 + (b % 3) for b in range(B)]
+        X = {k: torch.randn(B, k, device=ctx.dev).half() for k in (4096, 14336)}
+        Y = {r: torch.empty(B, r, device=ctx.dev, dtype=torch.float16) for r in (4096, 14336)}
+
+        def gemm():
+            for c in range(3):
+                for dm in blocks[c]:
+                    dm.gemm_mixedp(ps, X[dm.cols], out_dtype=torch.float16, stream=st)
+
+        def lut():
+            for c in range(3):
+                for dm in blocks[c]:
+                    gemv_batch([(dm, ps[b], X[dm.cols][b], Y[dm.rows][b]) for b in range(B)], st)
+
+        g_us = ctx.time_graph(gemm, reps=5) * 1e3 / 3
+        l_us = ctx.time_graph(lut, reps=5) * 1e3 / 3
+        pmax = max(ps)
+        plane_bytes = sum(pmax * r * k // 8 for _, r, k in shapes)
+        res[f"B{B}"] = {"gemm_us": round(g_us, 2), "lut_batched_us": round(l_us, 2),
+                        "gemm_plane_GBps": round(plane_bytes / (g_us * 1e-6) / 1e9, 1),
+                        "best": "gemm" if g_us < l_us else "lut_batched", "precisions": ps}
+    del blocks
+    res["what"] = ("us per MLP block (gate+up+down) at batch B with per-request p cycling 2,3,4; gemm = "
+                   "abcq_gemm_mixedp per matrix (tensor cores, planes read once up to max p); lut_batched = "
+                   "the B requests as B independent GEMVs in one abcq_gemv_batch launch per matrix")
+    return res
+
+
+def config4(ctx, args):
+    """BASELINE configs[3]: random-init Llama-3-8B decode step (32 layers, ctx
+    1024, batch 1), all linears AnyBCQ at p (q/k/v and gate/up row-stacked,
+    SiLU-gated down input), fp16 attention / norms / lm_head, vs the same step
+    with dense fp16 cuBLAS linears: tokens/s from CUDA-graph replays."""
+    torch = ctx.torch
+    from paper_2510_10467_b200.decode import Fp16LlamaStep, LlamaConfig, QuantizedLlamaStep, time_step
+    cfg = LlamaConfig(layers=32)
+    res = {"ctx": 1024, "layers": 32}
+    with torch.cuda.device(ctx.dev):
+        qm = QuantizedLlamaStep(cfg, p=3, ctx=1024, device=ctx.dev)
+        for p in PRECISIONS:
+            qm.p = p
+            ms = time_step(qm, 20)
+            gb = qm.linear_bytes() + cfg.vocab * cfg.hidden * 2
+            res[f"p{p}"] = {"ms_per_token": round(ms, 4), "tokens_per_s": round(1e3 / ms, 1),
+                            "weight_GBps": round(gb / (ms * 1e-3) / 1e9, 1)}
+        del qm
+        torch.cuda.empty_cache()
+        fm = Fp16LlamaStep(cfg, ctx=1024, device=ctx.dev)
+        ms = time_step(fm, 20)
+        res["fp16"] = {"ms_per_token": round(ms, 4), "tokens_per_s": round(1e3 / ms, 1)}
+        del fm
+        torch.cuda.empty_cache()
+    for p in PRECISIONS:
+        res[f"p{p}"]["speedup_vs_fp16"] = round(res["fp16"]["ms_per_token"] / res[f"p{p}"]["ms_per_token"], 2)
+    res["paper_table5_speedup"] = {"p2": round(245 / 105, 2), "p3": round(212 / 105, 2), "p4": round(186 / 105, 2)}
+    res["what"] = ("tokens/s of one batch-1 decode step captured as a CUDA graph; random weights and KV cache; "
+                   "paper Table 5 (PAPER.md:430-432) ratios beside")
+    return res
+
+
+def config5_row_sharded(ctx, args, peak):
+    """BASELINE configs[4]: Llama-3-70B layers (q/o 8192^2, k/v 1024x8192,
+    gate/up 28672x8192, down 8192x28672) at p=2 and p=4, output rows sharded
+    over the N ranks (RowShardedGemv: each rank's slice by one plan launch
+    straight into the NCCL all-gather buffer). Per layer set: the GEMVs alone
+    (graph of back-to-back launches) and GEMV + all-gather per layer (eager,
+    NCCL over NVLink), device time, max over ranks. Strong scaling: the total
+    work is fixed, each rank reads 1/N of the planes."""
+    torch = ctx.torch
+    import torch.distributed as dist
+    from paper_2510_10467_b200.parallel import RowShardedGemv, row_shard_bounds
+
+    world, rank = ctx.world, ctx.rank
+    engines = []
+    for li, (name, r, k) in enumerate(LAYERS_70B):
+        lo, hi = row_shard_bounds(r, world, rank)
+        dm = ctx.device_model(hi - lo, k, 2, 4, 50000 + 100 * li + rank) if hi > lo else None
+        engines.append(RowShardedGemv(shard=dm, rows=r, device=ctx.dev, dtype=torch.float16) if dm is not None
+                       else None)
+    xs = {k: torch.randn(k, device=ctx.dev).half() for k in (8192, 28672)}
+    for e in engines:
+        if e is not None:
+            e.x_buffer.copy_(xs[e.cols])
+    res = {"n_gpus": world}
+    for p in (2, 4):
+        def local_all():
+            for e in engines:
+                if e is not None:
+                    e.local(p, e.x_buffer, ctx.stream)
+
+        gemv_ms = ctx.time_graph(local_all, reps=10)
+        # + the all-gather of every layer's output (eager; the max over ranks)
+        with torch.cuda.stream(ctx.stream):
+            for _ in range(3):
+                for e in engines:
+                    e.local(p, e.x_buffer, ctx.stream)
+                    e.gather()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 10
+        with torch.cuda.stream(ctx.stream):
+            a.record(ctx.stream)
+            for _ in range(n):
+                for e in engines:
+                    e.local(p, e.x_buffer, ctx.stream)
+                    e.gather()
+            b.record(ctx.stream)
+        torch.cuda.synchronize()
+        full_ms = a.elapsed_time(b) / n
+        t = torch.tensor([gemv_ms, full_ms], device=ctx.dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gemv_ms, full_ms = (float(v) for v in t.tolist())
+        total = sum(algo_bytes(r, k, p) for _, r, k in LAYERS_70B)
+        res[f"p{p}"] = {"gemv_us_per_layer_set": round(gemv_ms * 1e3, 2),
+                        "gemv_allgather_us_per_layer_set": round(full_ms * 1e3, 2),
+                        "GBps_total": round(total / (gemv_ms * 1e-3) / 1e9, 1),
+                        "roofline_frac_per_gpu": round(total / world / (gemv_ms * 1e-3) / 1e9 / peak, 4)}
+    del engines
+    res["what"] = ("Llama-3-70B layer set (q,k,v,o,gate,up,down) row-sharded over n_gpus; GBps_total = the "
+                   "whole layer set's algorithmic bytes / GEMV time; all-gather of each layer's fp16 output")
+    return res
+
+
+# ---------------------------------------------------------------------------
+def _cpu_sample_models():
+    """The GPU step's exact host inputs (same splitmix64 words, f16-rounded
+    alphas and fp16 x as make_layer_models / run_gpu on rank 0, copy per
+    precision) for the C port."""
+    from oracle import anybcq_oracle as O  # checker / baseline only
+    out = {}
+    for pi, p in enumerate(PRECISIONS):
+        for li, (name, r, k) in enumerate(LAYERS):
+            seed = 1000 * pi + li
+            words = O.random_words(P_HI, r, k, seed=seed)
+            rng = np.random.default_rng(seed)
+            a = None
+            for q in range(P_LO, P_HI + 1):
+                aq = (0.01 + 0.1 * np.abs(rng.standard_normal((q, r, k // 128)))).astype(np.float32)
+                if q == p:
+                    a = aq.astype(np.float16).astype(np.float32)
+            out[(p, li)] = (words, a)
+    rng = np.random.default_rng(1234)
+    xs = {k: rng.standard_normal(k).astype(np.float16).astype(np.float64) for k in sorted({c for _, _, c in LAYERS})}
+    return out, xs
+
+
 def cpu_baseline(repeats: int = 2):
-    """The reference LUT algorithm (C port of gemv.py:67-95,188-222) on all host
-    cores, over the full layer sweep (the GPU step's workload), `repeats` times."""
+    """The reference LUT algorithm (C port of gemv.py:67-95,188-222) on the
+    GPU step's exact inputs: all host threads over the full step, and one
+    thread over a bounded sample (the step's q/k/v/o GEMVs at p=2)."""
     from oracle import c_oracle
 
     threads = c_oracle.cpu_threads()
-    models = _cpu_sample_models()
-    x = {k: np.random.default_rng(k).standard_normal(k).astype(np.float16).astype(np.float64)
-         for k in {c for _, _, c in LAYERS}}
-    for name, r, k, words, alphas in models[:1]:
-        c_oracle.lut_gemv(words, k, 128, alphas[2], None, 2, x[k], threads)  # warm
+    models, xs = _cpu_sample_models()
+    k0 = LAYERS[0][2]
+    c_oracle.lut_gemv(*models[(2, 0)][:1], k0, 128, models[(2, 0)][1], None, 2, xs[k0], threads)  # warm
     t0 = time.perf_counter()
     for _ in range(repeats):
-        for p in PRECISIONS:
-            for name, r, k, words, alphas in models:
-                c_oracle.lut_gemv(words, k, 128, alphas[p], None, p, x[k], threads)
+        for (p, li), (words, a) in models.items():
+            k = LAYERS[li][2]
+            c_oracle.lut_gemv(words, k, 128, a, None, p, xs[k], threads)
     dt = (time.perf_counter() - t0) / repeats
+    sample = [(2, li) for li in range(4)]
+    t0 = time.perf_counter()
+    for p, li in sample:
+        words, a = models[(p, li)]
+        k = LAYERS[li][2]
+        c_oracle.lut_gemv(words, k, 128, a, None, p, xs[k], 1)
+    dt1 = time.perf_counter() - t0
+    b1 = sum(algo_bytes(LAYERS[li][1], LAYERS[li][2], p) for p, li in sample)
     return {"value": round(step_bytes() / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "ms_per_step": round(dt * 1e3, 1),
-            "sample": f"full layer sweep (21 GEMVs) x{repeats}, C restatement of GemvEngine.lut, "
-                      f"{threads} pthreads"}
+            "cpu_model": cpu_model(), "ms_per_step": round(dt * 1e3, 1),
+            "sample": f"the full step's 21 GEMVs x{repeats} on the GPU step's exact inputs, C restatement of "
+                      f"GemvEngine.lut, {threads} pthreads",
+            "single_thread": {"value": round(b1 / dt1 / 1e9, 3), "unit": "GB/s", "cores": 1,
+                              "sample": "q/k/v/o at p=2 of the same inputs, 1 thread"}}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (C port) on this workload."""
+    """--impl reference: the reference's CPU algorithm (C port, all host threads)
+    on this workload -- the GPU step's exact inputs -- rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import c_oracle
 
     threads = c_oracle.cpu_threads()
-    models = _cpu_sample_models()
-    x = {k: np.random.default_rng(k).standard_normal(k).astype(np.float16).astype(np.float64)
-         for k in {c for _, _, c in LAYERS}}
+    models, xs = _cpu_sample_models()
 
     def one_step():
-        for p in PRECISIONS:
-            for name, r, k, words, alphas in models:
-                c_oracle.lut_gemv(words, k, 128, alphas[p], None, p, x[k], threads)
+        for (p, li), (words, a) in models.items():
+            k = LAYERS[li][2]
+            c_oracle.lut_gemv(words, k, 128, a, None, p, xs[k], threads)
 
     for _ in range(args.warmup):
         one_step()
@@ -634,18 +1006,27 @@ def run_reference(args):
         one_step()
     dt = (time.perf_counter() - t0) / args.steps
     value = round(step_bytes() / dt / 1e9, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "implementation": "reference CPU algorithm "
-                                        "(C restatement of GemvEngine.lut, all host threads)"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": "full layer sweep per step (C restatement of GemvEngine.lut; "
-                                   "reference is Python+numba, no compiled sources to build)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+        "dtype_note": DTYPE_NOTE, "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
+        "config": bench_config(world),
+        "implementation": "reference CPU algorithm (C restatement of GemvEngine.lut, all host threads); the "
+                          "reference is Python + numba with no compiled sources (its numba timing: config1.cpu)",
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": "the full step (21 GEMVs) per step, the GPU step's exact inputs"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
@@ -654,12 +1035,21 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
+    ap.add_argument("--sections", default="", help="comma list of the extra sections to run (default: all): "
+                    "variants,per_shape,fp16,batched8,e2e,config1,config3,config4,config5")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_gpu(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver launches
+        # N > 1 that way itself); fails if fewer GPUs are visible
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    run_gpu(args)
 
 
 if __name__ == "__main__":

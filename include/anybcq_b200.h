@@ -94,8 +94,9 @@ int abcq_device_check(int32_t dev);
 int abcq_debug_set_trace(void* d_buf);
 /* profiling experiments only (results are WRONG when mode is 1 or 2): 1 =
  * skip the table lookups, 2 = skip the weight loads; 23 = route single GEMVs
- * through the batch kernel instead of the cluster kernel; 5000 + 100*slots +
- * 10*C + t = force the cluster kernel's geometry (5000 = automatic). Default 0. */
+ * through the batch kernel instead of the cluster kernel; 27 = route every
+ * single GEMV through the cluster kernel; 5000 + 100*slots + 10*C + t = force
+ * the cluster kernel's geometry (C digit 6 = 16; 5000 = automatic). Default 0. */
 int abcq_debug_set_mode(int32_t mode);
 /* profiling aid: the launch geometry a single GEMV (abcq_gemv, or a batch of
  * one job) uses for this model and precision -- out7 = {cluster size C,
@@ -136,8 +137,11 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
 /* ---- GEMV: replaces GemvEngine.lut (gemv.py:188-222) ---------------------
  * y = sum_{i<p} alpha^(p)_{i,g} (B_i x) [+ offset^(p) . groupsum(x)]
  * for one request at precision p (runtime argument, no recompile).
- * x: (cols) in x_dtype; y: (rows) in y_dtype. TILED layout -> the sm_100a
- * LUT kernel; ROWMAJOR layout (any group size) -> the generic kernel.
+ * x: (cols) in x_dtype, 16-byte aligned (TILED); y: (rows) in y_dtype.
+ * TILED layout -> an sm_100a LUT kernel: the cluster kernel (split-K through
+ * distributed shared memory, one launch, no workspace use) for latency-bound
+ * GEMVs (<= 16 MiB of planes and <= 32 column slices), else the persistent
+ * streaming kernel; ROWMAJOR layout (any group size) -> the generic kernel.
  * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials + self-
  * resetting completion counters): zero-filled once before first use; may
  * not be shared by calls running concurrently (one workspace per stream).  */
@@ -148,7 +152,9 @@ int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype
 /* ---- batches of independent GEMVs ----------------------------------------
  * One persistent launch runs n_jobs GemvEngine.lut calls back to back (the
  * TMA stream never drains between them) -- e.g. q/k/v or gate/up of a
- * decoder layer, or several requests' precisions. All jobs: TILED layout,
+ * decoder layer, or several requests' precisions. Always the persistent
+ * streaming kernel, also for n_jobs == 1 (abcq_gemv instead takes the
+ * latency-path cluster kernel for small GEMVs). All jobs: TILED layout,
  * the same x/y/scale dtypes and mode; n_jobs <= abcq_gemv_batch_max_jobs().
  * Workspace: abcq_gemv_batch_workspace_bytes (the jobs' split-K partials,
  * then per-job self-resetting counters): zero-filled once per stream AND

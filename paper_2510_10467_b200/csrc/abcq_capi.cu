@@ -77,7 +77,7 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
-    if (mode >= 5000 && mode < 6000) {  // cluster GEMV geometry: 5000 + 100*slots + 10*C + tiles/warp (5000 = auto)
+    if (mode >= 5000 && mode < 6000) {  // cluster GEMV geometry: 5000 + 100*slots + 10*C + tiles/warp (5000 = auto; C digit 6 = 16)
         abcq::g_cl_force = mode - 5000;
         return 0;
     }

@@ -80,7 +80,7 @@ static bool plan(const abcq_model_t* m, int p, Geom& g) {
     // one or two CTAs per SM: two when a CTA's whole stream is short (its
     // producers then prefetch during the previous GEMV; the ring is smaller)
     const int64_t cta_bytes = (int64_t)Tm * ceil_div(NS, bc) * p * kBlockBytes;
-    int slots = forced_slots ? forced_slots : (cta_bytes <= 64 * 1024 ? 2 : 1);
+    int slots = forced_slots ? forced_slots : (cta_bytes <= 40 * 1024 ? 2 : 1);
     const int smem = slots == 2 ? kSmem2 : kSmem1;
     const int part_off = (int)(kTBase - kDynBase) + kTblBytes;
     const int Smax = (int)ceil_div(NS, bc);
@@ -154,7 +154,7 @@ bool cluster_supports(const abcq_model_t* m, int p) {
     // cluster kernel wins while a GEMV is latency-bound -- up to ~16 MB of plane
     // bytes and <= 2 slices per CTA at C = 16; larger GEMVs stream better
     // through the persistent batch kernel (more CTAs, deeper rings)
-    if (!g_cl_force) {
+    if (g_dbg_mode != 27) {  // (27: every single GEMV through the cluster kernel -- test coverage)
         const int64_t plane_bytes = (int64_t)p * tiled_plane_bytes(m->rows, m->cols);
         if (n_slices(m->cols) > 32 || plane_bytes > (int64_t)16 * 1024 * 1024) return false;
     }

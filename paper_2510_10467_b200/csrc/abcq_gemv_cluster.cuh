@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
     }
     __syncthreads();
     // the next kernel may launch now: with two CTAs per SM its producers fill
-    // their rings while this grid runs
-    pdl_launch_dependents();
+    // their rings while this grid runs (dbg 64: only once past the PDL wait)
+    if (!(a.dbg & 64)) pdl_launch_dependents();
 
     if (warp == kW) {
         // ---------------- producer: weights/scales never depend on the previous kernel
@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         };
 
         pdl_wait();  // x (and y) belong to the previous kernel
+        if (a.dbg & 64) pdl_launch_dependents();
         if (tid == 0) ABCQ_CTRACE(1);
         {
             // slices 0 and 1: x straight into registers and built at once;

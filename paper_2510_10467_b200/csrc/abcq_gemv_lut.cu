@@ -72,9 +72,6 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
                      int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st) {
-    // a single GEMV: one cluster launch, split-K completed through DSMEM
-    if (n == 1 && cluster_supports(models[0], ps[0]))
-        return launch_gemv_cluster(models[0], ps[0], xs[0], x_dtypes[0], ys[0], y_dtype, st);
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
     // fixed cost of a (job, slice) piece in blocks: measured best 300 for

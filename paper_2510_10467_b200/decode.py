@@ -121,6 +121,15 @@ class _Attention:
         return self.out
 
 
+def _persistent(m, p, x, out):
+    """One GEMV through the persistent batch kernel (a batch of one); other
+    linear objects (e.g. a dense test reference) through their own gemv()."""
+    if isinstance(m, DeviceModel):
+        gemv_batch([(m, p, x, out)])
+    else:
+        m.gemv(p, x, out=out)
+
+
 class QuantizedLlamaStep:
     """Decode step with AnyBCQ linears at precision p (p_lo..p_hi resident)."""
 
@@ -174,13 +183,17 @@ class QuantizedLlamaStep:
         resid = None
         for li, mats in enumerate(self.layers):
             add_rmsnorm(self.x, resid, self.norm_w[li][0], self.h, cfg.eps)
+            # q/k/v and o through the persistent batch kernel even as single jobs:
+            # between the step's other kernels it measured faster than the
+            # latency-path cluster kernel abcq_gemv takes for these shapes
+            # (p3: 2.19 vs 2.25 ms/token, tools/decode_ab.py)
             if self.stack_rows:
-                mats["qkv"].gemv(p, self.h, out=self.qkv)
+                _persistent(mats["qkv"], p, self.h, self.qkv)
             else:
                 gemv_batch([(mats["q"], p, self.h, self.q), (mats["k"], p, self.h, self.k),
                             (mats["v"], p, self.h, self.v)])
             a = self.attn(li, self.q, self.k, self.v)
-            mats["o"].gemv(p, a, out=self.o)
+            _persistent(mats["o"], p, a, self.o)
             add_rmsnorm(self.x, self.o, self.norm_w[li][1], self.h, cfg.eps)
             if self.stack_rows:  # y = [gate ; up]: exactly the down GEMV's SiLU-gated input layout
                 mats["gu"].gemv(p, self.h, out=self.gu)

@@ -53,45 +53,95 @@ def shard_model(model, lo: int, hi: int) -> MultiPrecisionModel:
 class RowShardedGemv:
     """y = W_p x with W's rows sharded over the ranks of `group`.
 
-    Every rank passes the same full model (or only its shard via
-    `shard=`), calls `gemv(p, x)` with the same x, and receives the full y.
-    `local_gemv(p, x_tensor) -> y_slice` defaults to the CUDA engine
-    (DeviceModel.gemv); tests inject a CPU oracle to cover the host logic.
+    Every rank passes the same full model (or only its shard, `shard=` with
+    `rows=` the full row count), calls `gemv(p, x)` with the same x, and
+    receives the full y. All buffers are allocated once: the rank's slice is
+    written by a GemvBatchPlan launch (one C-ABI call) straight into the
+    all-gather send buffer, and y is a view of the gather's receive buffer --
+    shards sit on 16-row tile boundaries with every rank but the last holding
+    exactly `pad_rows` rows, so the gathered buffer's first `rows` elements
+    ARE y in order (no per-call allocation, copy or concatenation).
+    `local_gemv(p, x_tensor) -> y_slice` replaces the CUDA engine (tests
+    inject a CPU oracle to cover the host logic with gloo).
     """
 
-    def __init__(self, model, group=None, *, scale_dtype="f16", device=None, local_gemv=None):
+    def __init__(self, model=None, group=None, *, scale_dtype="f16", device=None, local_gemv=None,
+                 dtype=torch.float16, shard=None, rows: int | None = None):
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.rows, self.cols = model.shape
+        if shard is not None:  # this rank's DeviceModel (or host model) only
+            if rows is None:
+                raise UsageError("shard= needs rows= (the full row count)")
+            self.rows, self.cols = int(rows), shard.cols if hasattr(shard, "cols") else shard.shape[1]
+        else:
+            self.rows, self.cols = model.shape
         self.lo, self.hi = row_shard_bounds(self.rows, self.world, self.rank)
         self.shard_rows = max(0, self.hi - self.lo)
         self.pad_rows = row_shard_bounds(self.rows, self.world, 0)[1]  # max shard size
-        self.shard = shard_model(model, self.lo, self.hi) if self.shard_rows else None
-        self.p_lo, self.p_hi = model.p_lo, model.p_hi
-        if local_gemv is None and self.shard is not None:
+        src = shard if shard is not None else model
+        self.p_lo, self.p_hi = src.p_lo, src.p_hi
+        self.dtype = dtype
+        self.dm = None
+        # this rank's rows of the model (host types; a DeviceModel when passed as shard=)
+        self.shard = shard if shard is not None else (shard_model(model, self.lo, self.hi) if self.shard_rows else None)
+        if local_gemv is None and self.shard_rows:
             from .device_model import DeviceModel
 
-            dm = DeviceModel.from_model(self.shard, scale_dtype=scale_dtype, device=device)
-            self.device = dm.device
-            local_gemv = lambda p, x: dm.gemv(p, x, out_dtype=x.dtype)  # noqa: E731
+            if isinstance(self.shard, DeviceModel):
+                self.dm = self.shard
+            else:
+                self.dm = DeviceModel.from_model(self.shard, scale_dtype=scale_dtype, device=device)
+            if self.dm.rows != self.shard_rows:
+                raise UsageError(f"shard has {self.dm.rows} rows, rank {self.rank} owns {self.shard_rows}")
+            self.device = self.dm.device
         else:
             self.device = torch.device(device) if device is not None else torch.device("cpu")
         self._local = local_gemv
+        self._send = torch.zeros(self.pad_rows, dtype=dtype, device=self.device)
+        self._recv = torch.empty(self.pad_rows * self.world, dtype=dtype, device=self.device)
+        self._x = torch.empty(self.cols, dtype=dtype, device=self.device)  # the plans' fixed input
+        self._plans = {}
 
-    def gemv(self, p: int, x: torch.Tensor) -> torch.Tensor:
+    def _plan(self, p: int):
+        plan = self._plans.get(p)
+        if plan is None:
+            from .device_model import GemvBatchPlan
+
+            plan = self._plans[p] = GemvBatchPlan([(self.dm, p, self._x, self._send[: self.shard_rows])])
+        return plan
+
+    def local(self, p: int, x: torch.Tensor, stream=None) -> None:
+        """This rank's slice of y into the send buffer (no communication)."""
         if not self.p_lo <= p <= self.p_hi:
             raise UsageError(f"precision {p} outside [{self.p_lo}, {self.p_hi}]")
         if x.numel() != self.cols:
             raise UsageError(f"input length {x.numel()} != cols {self.cols}")
-        out = torch.zeros(self.pad_rows, dtype=x.dtype, device=x.device)
-        if self.shard_rows:
-            out[: self.shard_rows] = self._local(p, x)
+        if not self.shard_rows:
+            return
+        if self._local is not None:
+            self._send[: self.shard_rows] = self._local(p, x)
+            return
+        if x.data_ptr() != self._x.data_ptr():
+            self._x.copy_(x.reshape(-1))
+        self._plan(p).launch(stream)
+
+    def gather(self, async_op: bool = False):
+        """All-gather the slices; y = self.y (a view of the receive buffer)."""
         if self.world == 1:
-            return out[: self.rows]
-        full = torch.empty(self.pad_rows * self.world, dtype=x.dtype, device=x.device)
-        dist.all_gather_into_tensor(full, out, group=self.group)
-        pieces = [full[r * self.pad_rows: r * self.pad_rows + (b[1] - b[0])]
-                  for r, b in enumerate(row_shard_bounds(self.rows, self.world, r)
-                                        for r in range(self.world))]
-        return torch.cat(pieces)
+            return None
+        return dist.all_gather_into_tensor(self._recv, self._send, group=self.group, async_op=async_op)
+
+    @property
+    def y(self) -> torch.Tensor:
+        return (self._send if self.world == 1 else self._recv)[: self.rows]
+
+    @property
+    def x_buffer(self) -> torch.Tensor:
+        """Write x here to skip the input copy of gemv()."""
+        return self._x
+
+    def gemv(self, p: int, x: torch.Tensor) -> torch.Tensor:
+        self.local(p, x)
+        self.gather()
+        return self.y

@@ -369,6 +369,7 @@ def test_cluster_gemv_geometries_vs_oracle(P, rows, cols, asym, sd):
             z = st.offset.astype(np.float16).astype(np.float32) if sd == "f16" else st.offset
         want[p] = O.gemv_lut(m.bitplanes.words, cols, 128, a, z, p, xf)
     try:
+        L.abcq_debug_set_mode(27)  # every shape through the cluster kernel
         for force in CLUSTER_FORCE:
             L.abcq_debug_set_mode(force)
             for p in (1, 2, 4, 5):
@@ -378,6 +379,7 @@ def test_cluster_gemv_geometries_vs_oracle(P, rows, cols, asym, sd):
                 assert torch.equal(y, dm.gemv(p, xd)), (force, p)   # bitwise repeatable
     finally:
         L.abcq_debug_set_mode(5000)
+        L.abcq_debug_set_mode(0)
 
 
 def test_gemv_batch_matches_single_calls(P):
@@ -667,3 +669,34 @@ def test_silu_glu_mixed_with_plain_jobs_in_one_batch(P):
     # an f32 job next to a gated one is rejected before any work
     arr[0].x_dtype = _lib.F32
     assert L.abcq_gemv_batch(arr, 3, ws.data_ptr(), ws.numel(), None) == _lib.E_ARG
+
+
+def test_row_sharded_gemv_nccl_world1(P):
+    """RowShardedGemv on the CUDA engine through a world-size-1 NCCL group:
+    the plan-launched shard GEMV lands in the gather buffer, y vs the oracle."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2510_10467_b200.parallel import RowShardedGemv
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        m = synth_model(P, 1000, 2048, 2, 4, seed=21)
+        eng = RowShardedGemv(m, scale_dtype="f16", device="cuda")
+        x = O.random_gaussian(1, 2048, seed=4).ravel().astype(np.float16)
+        xd = torch.from_numpy(x).cuda()
+        for p in (2, 3, 4):
+            y = eng.gemv(p, xd)
+            torch.cuda.synchronize()
+            a16 = m.scale_sets[p].alpha.astype(np.float16).astype(np.float32)
+            want = O.gemv_lut(m.bitplanes.words, 2048, 128, a16, None, p, x.astype(np.float32))
+            assert y.shape == (1000,) and O.rel_dev(y.float().cpu().numpy(), want) <= 1e-3
+        eng.gather()
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()

@@ -70,9 +70,10 @@ def _worker(rank, world, port, rows, cols, q):
                            sh.scale_sets[p].offset, p, xt.numpy())
             return torch.from_numpy(y.astype(np.float32))
 
-        eng = RowShardedGemv(m, local_gemv=lambda p, xt: local(p, xt, eng))
+        eng = RowShardedGemv(m, local_gemv=lambda p, xt: local(p, xt, eng), dtype=torch.float32)
         x = torch.from_numpy(O.random_gaussian(1, cols, 3).ravel())
-        y = eng.gemv(2, x)
+        y = eng.gemv(2, x).clone()
+        assert eng.gemv(2, x).data_ptr() == eng.y.data_ptr()   # preallocated: y is the gather buffer
         want = O.gemv_lut(m.bitplanes.words, cols, 128, m.scale_sets[2].alpha, m.scale_sets[2].offset, 2, x.numpy())
         q.put((rank, float(np.max(np.abs(y.numpy() - want.astype(np.float32)))), tuple(y.shape)))
     finally:

@@ -141,6 +141,7 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
              "us_batch_kernel": round(t_old, 3)}
         if a.sweep:
             sw = {}
+            L.abcq_debug_set_mode(27)
             for slots in (1, 2):
                 for Cc in (8, 6):
                     for tcw in (2,):
@@ -157,6 +158,7 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
                         except Exception as e:  # noqa: BLE001
                             sw[f"s{slots}C{Cc}t{tcw}"] = str(e)[:80]
             L.abcq_debug_set_mode(5000)
+            L.abcq_debug_set_mode(0)
             r["sweep"] = sw
         rec[f"p{p}"] = r
         print(rows, cols, p, json.dumps(r), flush=True)

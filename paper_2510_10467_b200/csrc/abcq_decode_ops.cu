@@ -342,7 +342,7 @@ __global__ void silu_mul_kernel(const __half* __restrict__ g, const __half* __re
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         const float gv = __half2float(g[i]);
-        a[i] = __float2half_rn(gv / (1.f + __expf(-gv)) * __half2float(u[i]));
+        a[i] = __float2half_rn(__fdividef(gv, 1.f + __expf(-gv)) * __half2float(u[i]));
     }
 }
 

@@ -85,7 +85,7 @@ static bool plan(const abcq_model_t* m, int p, Geom& g) {
     const int part_off = (int)(kTBase - kDynBase) + kTblBytes;
     const int Smax = (int)ceil_div(NS, bc);
     const int xs_off = part_off + part_bytes;
-    const int xs_bytes = Smax > 2 ? (Smax - 2) * kSliceCols * 4 : 0;
+    const int xs_bytes = Smax * kSliceCols * 4;
     const int recv_off = xs_off + xs_bytes;
     const int recv_bytes = bc > 1 ? (Tm * 16 + 8) * 4 : 0;
     const int ring_off = (recv_off + recv_bytes + 127) / 128 * 128;

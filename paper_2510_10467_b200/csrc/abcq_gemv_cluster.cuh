@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         const uint32_t cs = ASYM ? csum_lo : 0u;
         // build slice sl's table into segment sl & 1 from the staged x
         auto build = [&](int sl) {
-            const uint32_t xv = xs_lo + (uint32_t)(((sl - 2) * kSliceCols + cp * 16) * 4);
+            const uint32_t xv = xs_lo + (uint32_t)((sl * kSliceCols + cp * 16) * 4);
             const float4 v0 = lds_v4f(xv), v1 = lds_v4f(xv + 16), v2 = lds_v4f(xv + 32), v3 = lds_v4f(xv + 48);
             const float pa[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             const float pb[8] = {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
@@ -311,30 +311,25 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         if (a.dbg & 64) pdl_launch_dependents();
         if (tid == 0) ABCQ_CTRACE(1);
         {
-            // slices 0 and 1: x straight into registers and built at once;
-            // slices 2..S-1: x staged in shared memory (f32) for the later builds
-            float xa[8], xb[8], na[8], nb[8];
-            const bool dox = !(a.dbg & 32);
-            if (S > 0 && dox) slice_x16<XT>(a, s0, cp, xa, xb);
-            if (S > 1 && dox) slice_x16<XT>(a, s0 + 1, cp, na, nb);
-            const int nq = (S - 2) * kChunksPerSlice;
+            // x of the CTA's slices -> shared memory (f32): one loop (one copy
+            // of the f16 / f32 / SiLU-gated load code), every load in flight
+            const int nq = S * kChunksPerSlice;
             const XT* xg = static_cast<const XT*>(a.x);
 #pragma unroll 1
-            for (int q = tid; q < (dox ? nq : 0); q += kW * 32) {
+            for (int q = tid; q < ((a.dbg & 32) ? 0 : nq); q += kW * 32) {
                 float xq[8];
-                load_x8_any<XT>(xg, (s0 + 2) * kSliceCols + q * 8, a.cols, a.glu, xq);
+                load_x8_any<XT>(xg, s0 * kSliceCols + q * 8, a.cols, a.glu, xq);
                 const uint32_t d = xs_lo + (uint32_t)(q * 32);
                 sts_v2(d, xq[0], xq[1]);
                 sts_v2(d + 8, xq[2], xq[3]);
                 sts_v2(d + 16, xq[4], xq[5]);
                 sts_v2(d + 24, xq[6], xq[7]);
             }
-            if (tid == 0) ABCQ_CTRACE(9);
-            if (!(a.dbg & 4)) {
-                if (S > 0) build_cols2(xa, xb, u, cp, tbl_lo, 0, cs);
-                if (S > 1) build_cols2(na, nb, u, cp, tbl_lo, 1, cs);
-            }
         }
+        bar_consumers();
+        if (tid == 0) ABCQ_CTRACE(9);
+#pragma unroll 1
+        for (int sl = 0; sl < S && sl < 2 && !(a.dbg & 4); ++sl) build(sl);
         bar_consumers();
         if (tid == 0) ABCQ_CTRACE(2);
 
@@ -381,35 +376,17 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
                 const uint32_t q0 = (uint32_t)(v0 ? warp : 0), q1 = (uint32_t)(v1 ? warp + kW : 0);
                 float acc0 = 0.f, acc1 = 0.f;
                 mbar_wait(&full[slot], ph);
-                if (tid == 0 && a.trace) {
-                    if (sl == 0 && k == 0) ABCQ_CTRACE(5);
-                    ABCQ_CTRACE(7);
-                }
                 const uint32_t st = ring_lo + (uint32_t)(slot * a.stage_bytes);
                 if ((a.dbg & 1) == 0 && v0) {
-                    if (v1) {  // two tiles x two planes per group
+                    // two tiles x two planes per group (one code path: a warp
+                    // without a second tile looks up a duplicate, discarded)
 #pragma unroll 1
-                        for (int i = 0; i < p; i += 2) {
-                            const bool pv = i + 1 < p;
-                            const uint32_t i1 = pv ? i + 1 : i;
-                            const uint32_t qq[4] = {q0, q1, q0, q1}, ii[4] = {(uint32_t)i, (uint32_t)i, i1, i1};
-                            const bool vv[4] = {true, true, pv, pv}, t1[4] = {false, true, false, true};
-                            group4(st, qq, ii, vv, t1, acc0, acc1);
-                        }
-                    } else {  // one tile x four planes per group
-#pragma unroll 1
-                        for (int i = 0; i < p; i += 4) {
-                            uint32_t ii[4];
-                            bool vv[4];
-#pragma unroll
-                            for (int b = 0; b < 4; ++b) {
-                                vv[b] = i + b < p;
-                                ii[b] = vv[b] ? (uint32_t)(i + b) : (uint32_t)i;
-                            }
-                            const uint32_t qq[4] = {q0, q0, q0, q0};
-                            const bool t1[4] = {false, false, false, false};
-                            group4(st, qq, ii, vv, t1, acc0, acc1);
-                        }
+                    for (int i = 0; i < p; i += 2) {
+                        const bool pv = i + 1 < p;
+                        const uint32_t i1 = pv ? i + 1 : i;
+                        const uint32_t qq[4] = {q0, q1, q0, q1}, ii[4] = {(uint32_t)i, (uint32_t)i, i1, i1};
+                        const bool vv[4] = {true, v1, pv, v1 && pv}, t1[4] = {false, true, false, true};
+                        group4(st, qq, ii, vv, t1, acc0, acc1);
                     }
                     if constexpr (ASYM) {  // + offset . group sum of x, after the planes
                         acc0 = fmaf(lds_scale<ST>(st + zoff + (q0 * 32 + lane) * (uint32_t)sizeof(ST)), gx, acc0);

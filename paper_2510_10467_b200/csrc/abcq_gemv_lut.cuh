@@ -114,7 +114,7 @@ __device__ __forceinline__ void load_x8(const XT* x, int k0, int cols, float (&x
 // the same expression as silu_mul_kernel (abcq_decode_ops.cu) -> bitwise equal
 __device__ __forceinline__ float silu_glu(__half g, __half u) {
     const float gv = __half2float(g);
-    return __half2float(__float2half_rn(gv / (1.f + __expf(-gv)) * __half2float(u)));
+    return __half2float(__float2half_rn(__fdividef(gv, 1.f + __expf(-gv)) * __half2float(u)));
 }
 
 template <typename XT>

@@ -50,4 +50,9 @@ summary = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py")
     "launches": len(main), "time_share": share,
     "source": f"profiles/{tag}_launches.csv (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum)"},
     indent=1) + "\n")
+cl_rep = ROOT / "gpurun_out" / f"prof_cl_{tag}.ncu-rep"
+if cl_rep.exists():  # the cluster single-GEMV kernel (abcq_gemv latency path)
+    cl = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(cl_rep), "--top", "30"],
+                        capture_output=True, text=True).stdout
+    (out / f"{tag}_gemv_cluster_ncu_full.txt").write_text(cl)
 print(json.dumps(share), round(traffic))

@@ -435,6 +435,8 @@ def run_gpu(args):
             out["config3"] = config3(ctx)
         if want("config4"):
             out["config4"] = config4(ctx, args)
+        if want("quantizer"):
+            out["quantizer"] = quantizer_section(ctx, args)
     if mp:
         dist.barrier()
 
@@ -928,6 +930,50 @@ def config5_row_sharded(ctx, args, peak):
     return res
 
 
+def quantizer_section(ctx, args):
+    """The GPU quantizer: build_multiprecision 2:4,
+    group 128, cycles 1 (the reference CLI's bench-suite fit, cli.py:150-152)
+    on Llama-3-8B shapes, wall time with the device synchronised, the
+    relative errors per precision; beside it the unmodified reference
+    (baseline/_ref, numpy f64 on the host) on the 4096x4096 matrix."""
+    torch = ctx.torch
+    from paper_2510_10467_b200.model import QuantConfig
+    from paper_2510_10467_b200.quantize import build_multiprecision, precision_errors
+    from paper_2510_10467_b200.tensor_io import random_gaussian
+
+    cfg = QuantConfig(group_size=128, cycles=1)
+    build_multiprecision(random_gaussian(64, 256, seed=1), 2, 4, cfg)  # (module load, first launches)
+    res = {}
+    for r, k in ((4096, 4096), (14336, 4096)):
+        w = random_gaussian(r, k, seed=0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = build_multiprecision(w, 2, 4, cfg)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        errs = precision_errors(w, m)
+        res[f"{r}x{k}"] = {"gpu_s": round(dt, 3), "relative_sq_error": {p: round(e, 6) for p, e in errs.items()}}
+    ref = ROOT / "baseline" / "_ref"
+    if not args.no_cpu and (ref / "anybcq").exists():
+        code = ("import time, json\n"
+                "from anybcq import QuantConfig, random_gaussian\n"
+                "from anybcq.progressive import build_multiprecision, precision_errors\n"
+                "w = random_gaussian(4096, 4096, seed=0)\n"
+                "t0 = time.perf_counter(); m = build_multiprecision(w, 2, 4, QuantConfig(group_size=128, cycles=1))\n"
+                "dt = time.perf_counter() - t0\n"
+                "print(json.dumps({'cpu_s': round(dt, 2), 'relative_sq_error': {p: round(e, 6) for p, e in "
+                "precision_errors(w, m).items()}}))\n")
+        try:
+            r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=str(ref)),
+                               capture_output=True, text=True, timeout=600)
+            res["reference_4096x4096"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:  # noqa: BLE001
+            res["reference_4096x4096"] = f"failed: {str(exc)[:100]}"
+    res["what"] = ("build_multiprecision(w, 2, 4, group 128, cycles 1): GPU quantizer wall seconds (device "
+                   "synchronised) and relative squared errors; the unmodified reference on the host beside it")
+    return res
+
+
 # ---------------------------------------------------------------------------
 def _cpu_sample_models():
     """The GPU step's exact host inputs (same splitmix64 words, f16-rounded
@@ -1037,7 +1083,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
     ap.add_argument("--sections", default="", help="comma list of the extra sections to run (default: all): "
-                    "variants,per_shape,fp16,batched8,e2e,config1,config3,config4,config5")
+                    "variants,per_shape,fp16,batched8,e2e,config1,config3,config4,config5,quantizer")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

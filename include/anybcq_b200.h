@@ -195,6 +195,36 @@ int abcq_gemv_naive(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x
  * half-precision (cuBLAS) comparison weights.                              */
 int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype, void* stream);
 
+/* ---- BCQ fitting: replaces the reference's f64 fitting internals ----------
+ * (the producer of the planes and scale sets above). All
+ * device buffers; w (rows, cols) f64; codes (q, rows, cols) int8 of -1/+1
+ * (plane-major, the reference's internal form before pack_signs); alpha
+ * (q, rows, G) and offset (rows, G) f64, G = ceil(cols / group_size);
+ * group_size <= 1024, 1 <= q <= ABCQ_MAX_PLANES.
+ *   abcq_fit_greedy   _greedy64 (bcq.py:160-180): asymmetric offset = group
+ *                     mean; plane i = sign(residual) (0 -> +1), alpha_i = mean
+ *                     |residual| per group. d_scratch: rows*cols f64.
+ *   abcq_fit_ls       _ls64 + _solve_psd_batch (bcq.py:183-230): per-group
+ *                     least squares over alpha (+ offset), planes fixed, with
+ *                     the reference's eigenvalue ridge rule (RANK_CUTOFF
+ *                     1e-10, RIDGE_SCALE 1e-8); *d_ridged |= 1 if any group
+ *                     was ridged.
+ *   abcq_fit_bs       _bs_codes64 (bcq.py:269-295): each code set to the
+ *                     nearest of the 2^q levels (ties to the larger level).
+ *   abcq_fit_residual_sign  expand_step's new plane (progressive.py:124-127):
+ *                     sign(w - dequant(codes[:q], alpha[:q], offset)).      */
+int abcq_fit_greedy(const double* d_w, int32_t rows, int32_t cols, int32_t group_size, int32_t q,
+                    int32_t asymmetric, int8_t* d_codes, double* d_alpha, double* d_offset, double* d_scratch,
+                    void* stream);
+int abcq_fit_ls(const double* d_w, const int8_t* d_codes, int32_t q, int32_t rows, int32_t cols,
+                int32_t group_size, int32_t asymmetric, double* d_alpha, double* d_offset, int32_t* d_ridged,
+                void* stream);
+int abcq_fit_bs(const double* d_w, const double* d_alpha, const double* d_offset, int32_t q, int32_t rows,
+                int32_t cols, int32_t group_size, int8_t* d_codes, void* stream);
+int abcq_fit_residual_sign(const double* d_w, const int8_t* d_codes, const double* d_alpha, const double* d_offset,
+                           int32_t q, int32_t rows, int32_t cols, int32_t group_size, int8_t* d_plane,
+                           void* stream);
+
 /* ---- decode-step harness ops (not part of the reference boundary) --------
  * The non-GEMV ops of the Llama-3 decode step (paper_2510_10467_b200/decode.py,
  * SURVEY §8f rank 3), fused, all fp16 tensors with f32 math:

@@ -23,4 +23,8 @@ def __getattr__(name):
     if name in ("DeviceModel", "GemvBatchPlan", "gemv_batch"):
         from . import device_model
         return getattr(device_model, name)
+    if name in ("QuantizedMatrix", "greedy_init", "ls_update_scales", "bs_recalibrate_codes", "alternate_fit",
+                "expand_step", "build_multiprecision", "precision_errors", "relative_reconstruction_error"):
+        from . import quantize
+        return getattr(quantize, name)
     raise AttributeError(name)

@@ -69,6 +69,10 @@ SIGNATURES = {
     "abcq_debug_set_trace": (C.c_int, [_vp]),
     "abcq_debug_set_mode": (C.c_int, [_i32]),
     "abcq_debug_gemv_geometry": (C.c_int, [_PM, _i32, C.POINTER(_i32)]),
+    "abcq_fit_greedy": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "abcq_fit_ls": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "abcq_fit_bs": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "abcq_fit_residual_sign": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "abcq_tiled_plane_bytes": (C.c_int, [_i32, _i32, C.POINTER(_i64)]),
     "abcq_tiled_scale_elems": (C.c_int, [_i32, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)]),
     "abcq_pack_planes": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),

@@ -303,6 +303,48 @@ int abcq_dequantize(const abcq_model_t* m, int32_t p, void* d_w, int32_t w_dtype
 }
 
 // ---- decode-step harness ops -------------------------------------------------
+static int check_fit(int rows, int cols, int g, int q, const void* w) {
+    if (!w || rows < 1 || cols < 1) return fail(ABCQ_E_ARG, "fit: bad matrix");
+    if (g < 1 || g > 1024) return fail(ABCQ_E_ARG, "fit: group_size %d outside [1, 1024]", g);
+    if (q < 1 || q > ABCQ_MAX_PLANES) return fail(ABCQ_E_PRECISION, "fit: plane count %d outside [1, %d]", q, ABCQ_MAX_PLANES);
+    return 0;
+}
+
+int abcq_fit_greedy(const double* d_w, int32_t rows, int32_t cols, int32_t group_size, int32_t q, int32_t asymmetric,
+                    int8_t* d_codes, double* d_alpha, double* d_offset, double* d_scratch, void* stream) {
+    if (int rc = check_fit(rows, cols, group_size, q, d_w)) return rc;
+    if (!d_codes || !d_alpha || !d_scratch || (asymmetric && !d_offset)) return fail(ABCQ_E_ARG, "abcq_fit_greedy: bad outputs");
+    return cuda_ret(abcq::launch_fit_greedy(d_w, rows, cols, group_size, q, asymmetric != 0, d_codes, d_alpha, d_offset,
+                                            d_scratch, (cudaStream_t)stream),
+                    "abcq_fit_greedy");
+}
+
+int abcq_fit_ls(const double* d_w, const int8_t* d_codes, int32_t q, int32_t rows, int32_t cols, int32_t group_size,
+                int32_t asymmetric, double* d_alpha, double* d_offset, int32_t* d_ridged, void* stream) {
+    if (int rc = check_fit(rows, cols, group_size, q, d_w)) return rc;
+    if (!d_codes || !d_alpha || !d_ridged || (asymmetric && !d_offset)) return fail(ABCQ_E_ARG, "abcq_fit_ls: bad buffers");
+    return cuda_ret(abcq::launch_fit_ls(d_w, d_codes, q, rows, cols, group_size, asymmetric != 0, d_alpha, d_offset,
+                                        d_ridged, (cudaStream_t)stream),
+                    "abcq_fit_ls");
+}
+
+int abcq_fit_bs(const double* d_w, const double* d_alpha, const double* d_offset, int32_t q, int32_t rows, int32_t cols,
+                int32_t group_size, int8_t* d_codes, void* stream) {
+    if (int rc = check_fit(rows, cols, group_size, q, d_w)) return rc;
+    if (!d_alpha || !d_codes) return fail(ABCQ_E_ARG, "abcq_fit_bs: bad buffers");
+    return cuda_ret(abcq::launch_fit_bs(d_w, d_alpha, d_offset, q, rows, cols, group_size, d_codes, (cudaStream_t)stream),
+                    "abcq_fit_bs");
+}
+
+int abcq_fit_residual_sign(const double* d_w, const int8_t* d_codes, const double* d_alpha, const double* d_offset,
+                           int32_t q, int32_t rows, int32_t cols, int32_t group_size, int8_t* d_plane, void* stream) {
+    if (int rc = check_fit(rows, cols, group_size, q, d_w)) return rc;
+    if (!d_codes || !d_alpha || !d_plane) return fail(ABCQ_E_ARG, "abcq_fit_residual_sign: bad buffers");
+    return cuda_ret(abcq::launch_fit_residual_sign(d_w, d_codes, d_alpha, d_offset, q, rows, cols, group_size, d_plane,
+                                                   (cudaStream_t)stream),
+                    "abcq_fit_residual_sign");
+}
+
 int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
                          void* stream) {
     if (!d_x || !d_w || !d_y || n < 1 || n > 8192) return fail(ABCQ_E_ARG, "abcq_add_rmsnorm_f16: bad arguments");

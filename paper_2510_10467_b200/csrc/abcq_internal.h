@@ -60,6 +60,16 @@ int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads,
                        float scale, void* out, void* ws, cudaStream_t st);
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st);
 
+// BCQ fitting (abcq_quantize.cu), f64, codes int8 (q, rows, cols)
+int launch_fit_greedy(const double* w, int rows, int cols, int g, int q, int asym, int8_t* codes, double* alpha,
+                      double* offset, double* scratch, cudaStream_t st);
+int launch_fit_ls(const double* w, const int8_t* codes, int q, int rows, int cols, int g, int asym, double* alpha,
+                  double* offset, int* ridged, cudaStream_t st);
+int launch_fit_bs(const double* w, const double* alpha, const double* offset, int q, int rows, int cols, int g,
+                  int8_t* codes, cudaStream_t st);
+int launch_fit_residual_sign(const double* w, const int8_t* codes, const double* alpha, const double* offset, int q,
+                             int rows, int cols, int g, int8_t* plane, cudaStream_t st);
+
 extern unsigned long long* g_trace;
 extern int g_dbg_mode;
 extern int g_piece_blocks;

@@ -120,7 +120,8 @@ class BitPlaneSet:
         return np.ascontiguousarray(self.words, dtype="<u4").tobytes()
 
     def __eq__(self, other) -> bool:
-        if not isinstance(other, BitPlaneSet):
+        # duck-typed: equal to the reference's BitPlaneSet with the same words too
+        if not all(hasattr(other, a) for a in ("planes", "rows", "cols", "words")):
             return NotImplemented
         return ((self.planes, self.rows, self.cols) == (other.planes, other.rows, other.cols)
                 and np.array_equal(self.words, other.words))
@@ -156,6 +157,16 @@ class ScaleTensor:
     @property
     def groups(self) -> int:
         return self.alpha.shape[2]
+
+    def __eq__(self, other) -> bool:
+        # bcq.py:87-96, duck-typed (a reference ScaleTensor with equal arrays is equal)
+        if not all(hasattr(other, a) for a in ("alpha", "offset", "group_size")):
+            return NotImplemented
+        if self.group_size != other.group_size or not np.array_equal(self.alpha, other.alpha):
+            return False
+        if (self.offset is None) != (other.offset is None):
+            return False
+        return self.offset is None or np.array_equal(self.offset, other.offset)
 
 
 @dataclass(frozen=True, eq=False)

@@ -4,7 +4,8 @@ drop-in before the reference's own test modules import it.
 Loaded with `-p ref_dropin_plugin` by tests/test_reference_suite_gpu.py, which
 runs the reference's unchanged test files (installed under baseline/_ref by
 tools/install_reference.sh) on the B200 engine. This is the reference-side
-binding a maintainer would add: the engine class and bench() are swapped, and the drop-in's
+binding a maintainer would add: the engine class, bench() and the fitting API
+(the GPU quantizer) are swapped, and the drop-in's
 argument errors surface as the reference's own anybcq.UsageError (the
 reference's CLI exit codes and HTTP 400 mapping catch that class,
 cli.py:247-266, service/server.py:107-109).
@@ -16,9 +17,13 @@ import anybcq
 import anybcq.cli
 import anybcq.errors
 import anybcq.gemv
+import anybcq.bcq
+import anybcq.progressive
 import anybcq.service.server
 
 import paper_2510_10467_b200.engine as b200
+import paper_2510_10467_b200.quantize as b200q
+from paper_2510_10467_b200.errors import NonFiniteError as B200NonFiniteError
 from paper_2510_10467_b200.errors import UsageError as B200UsageError
 
 
@@ -29,6 +34,8 @@ def _ref_errors(fn):
             return fn(*a, **k)
         except B200UsageError as exc:
             raise anybcq.errors.UsageError(str(exc)) from exc
+        except B200NonFiniteError as exc:
+            raise anybcq.errors.NonFiniteError(str(exc)) from exc
     return wrapped
 
 
@@ -54,3 +61,11 @@ for _mod in (anybcq, anybcq.gemv, anybcq.cli, anybcq.service.server):
 for _mod in (anybcq, anybcq.gemv):
     _mod.gemv_lut = gemv_lut
     _mod.gemv_naive = gemv_naive
+
+# the GPU quantizer (quantize.py) behind the reference's fitting API
+for _name in ("greedy_init", "ls_update_scales", "bs_recalibrate_codes", "alternate_fit", "dequantize",
+              "expand_step", "build_multiprecision", "precision_errors"):
+    _fn = _ref_errors(getattr(b200q, _name))
+    for _mod in (anybcq, anybcq.bcq, anybcq.progressive, anybcq.cli):
+        if hasattr(_mod, _name):
+            setattr(_mod, _name, _fn)

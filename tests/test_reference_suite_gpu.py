@@ -2,9 +2,11 @@
 drop-in engine (VERDICT r1 "the reference's own test suite through
 the drop-in"): tests/test_gemv.py, acceptance criteria C6 (path equivalence)
 and C7 (traffic law), the CLI gemv/bench tests and the service's per-request
-precision / bench tests. GemvEngine / gemv_lut / gemv_naive of the installed
-reference (baseline/_ref, tools/install_reference.sh) are replaced by this
-repo's (tests/ref_dropin_plugin.py) before the test modules import them.
+precision / bench tests; and the fitting tests (test_bcq_core.py,
+test_progressive.py, the CLI quantize tests) on the GPU quantizer.
+GemvEngine / gemv_lut / gemv_naive / bench and the fitting API of the
+installed reference (baseline/_ref, tools/install_reference.sh) are replaced
+by this repo's (tests/ref_dropin_plugin.py) before the test modules import them.
 Skips when baseline/_ref is absent."""
 
 import os
@@ -29,7 +31,9 @@ TESTS = REF / "anybcq_tests"
 SELECTION = [
     ("test_gemv.py", "not test_latency_scales_with_precision"),
     ("test_acceptance.py", "criterion_06 or criterion_07"),
-    ("test_cli.py", "gemv or bench"),
+    ("test_cli.py", "gemv or bench or quantize"),
+    ("test_bcq_core.py", None),
+    ("test_progressive.py", None),
     ("test_service.py", "gemv or bench or health or listing"),
 ]
 

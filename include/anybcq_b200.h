@@ -242,7 +242,10 @@ int abcq_fit_residual_sign(const double* d_w, const int8_t* d_codes, const doubl
  *                (the last split block combines) at a fixed offset, so one
  *                workspace serves every pos, in any order, and the separate
  *                attn_decode path
- *   silu_mul:    a = silu(g) * u                                            */
+ *   silu_mul:    a = silu(g) * u
+ *   argmax:      *out = index of the largest of n f16 values (first on ties,
+ *                as torch.argmax); the workspace (abcq_argmax_workspace_bytes)
+ *                is zero-filled once (a self-resetting completion counter) */
 int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
                          void* stream);
 int abcq_rope_append_f16(void* d_q, void* d_k, const void* d_v, const float* d_cos, const float* d_sin,
@@ -257,6 +260,9 @@ int abcq_rope_attn_decode_f16(const void* d_q, const void* d_k, const void* d_v,
                               int32_t max_ctx, int32_t pos, float scale, void* d_out, void* d_workspace,
                               size_t workspace_bytes, void* stream);
 int abcq_silu_mul_f16(const void* d_g, const void* d_u, void* d_a, int32_t n, void* stream);
+int abcq_argmax_workspace_bytes(size_t* out_bytes);
+int abcq_argmax_f16(const void* d_x, int32_t n, int64_t* d_out, void* d_workspace, size_t workspace_bytes,
+                    void* stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,8 @@ SIGNATURES = {
     "abcq_debug_set_trace": (C.c_int, [_vp]),
     "abcq_debug_set_mode": (C.c_int, [_i32]),
     "abcq_debug_gemv_geometry": (C.c_int, [_PM, _i32, C.POINTER(_i32)]),
+    "abcq_argmax_workspace_bytes": (C.c_int, [C.POINTER(_sz)]),
+    "abcq_argmax_f16": (C.c_int, [_vp, _i32, _vp, _vp, _sz, _vp]),
     "abcq_fit_greedy": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "abcq_fit_ls": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "abcq_fit_bs": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),

@@ -345,6 +345,21 @@ int abcq_fit_residual_sign(const double* d_w, const int8_t* d_codes, const doubl
                     "abcq_fit_residual_sign");
 }
 
+int abcq_argmax_workspace_bytes(size_t* out_bytes) {
+    if (!out_bytes) return fail(ABCQ_E_ARG, "out_bytes is NULL");
+    *out_bytes = abcq::argmax_workspace_bytes();
+    return 0;
+}
+
+int abcq_argmax_f16(const void* d_x, int32_t n, int64_t* d_out, void* d_workspace, size_t workspace_bytes,
+                    void* stream) {
+    if (!d_x || !d_out || n < 1) return fail(ABCQ_E_ARG, "abcq_argmax_f16: bad arguments");
+    if (!d_workspace || workspace_bytes < abcq::argmax_workspace_bytes())
+        return fail(ABCQ_E_WORKSPACE, "abcq_argmax_f16: workspace too small");
+    return cuda_ret(abcq::launch_argmax(d_x, n, reinterpret_cast<long long*>(d_out), d_workspace, (cudaStream_t)stream),
+                    "abcq_argmax_f16");
+}
+
 int abcq_add_rmsnorm_f16(void* d_x, const void* d_residual, const void* d_w, void* d_y, int32_t n, float eps,
                          void* stream) {
     if (!d_x || !d_w || !d_y || n < 1 || n > 8192) return fail(ABCQ_E_ARG, "abcq_add_rmsnorm_f16: bad arguments");

@@ -396,6 +396,72 @@ int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads,
                            splits, static_cast<__half*>(out));
 }
 
+// argmax over n f16 values (the decode step's greedy token): every block
+// reduces a grid-stride share to (max, first index), the last block to finish
+// (a self-resetting counter in the workspace) reduces the block results; ties
+// resolve to the smallest index, as torch.argmax
+constexpr int kArgmaxBlocks = 128;
+__device__ __forceinline__ void argmax_pair(float& v, int& i, float v2, int i2) {
+    if (v2 > v || (v2 == v && i2 < i)) {
+        v = v2;
+        i = i2;
+    }
+}
+__global__ void __launch_bounds__(256) argmax_kernel(const __half* __restrict__ x, int n, long long* __restrict__ out,
+                                                     float* __restrict__ bv, int* __restrict__ bi,
+                                                     unsigned* __restrict__ cnt) {
+    pdl_enter();
+    __shared__ float sv[8];
+    __shared__ int si[8];
+    __shared__ bool last;
+    float v = -INFINITY;
+    int i = 0x7fffffff;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        argmax_pair(v, i, __half2float(x[k]), k);
+    auto block_reduce = [&]() {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) argmax_pair(v, i, __shfl_xor_sync(0xffffffffu, v, o), __shfl_xor_sync(0xffffffffu, i, o));
+        if ((threadIdx.x & 31) == 0) {
+            sv[threadIdx.x >> 5] = v;
+            si[threadIdx.x >> 5] = i;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) argmax_pair(v, i, sv[w], si[w]);
+    };
+    block_reduce();
+    if (threadIdx.x == 0) {
+        bv[blockIdx.x] = v;
+        bi[blockIdx.x] = i;
+        __threadfence();
+        last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    v = -INFINITY;
+    i = 0x7fffffff;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) argmax_pair(v, i, __ldcg(bv + b), __ldcg(bi + b));
+    __syncthreads();
+    block_reduce();
+    if (threadIdx.x == 0) {
+        *out = i;
+        *cnt = 0u;  // self-reset for the next launch
+    }
+}
+
+size_t argmax_workspace_bytes() { return kArgmaxBlocks * (sizeof(float) + sizeof(int)) + 128; }
+
+int launch_argmax(const void* x, int n, long long* out, void* ws, cudaStream_t st) {
+    char* w = static_cast<char*>(ws);
+    unsigned* cnt = reinterpret_cast<unsigned*>(w);
+    float* bv = reinterpret_cast<float*>(w + 128);
+    int* bi = reinterpret_cast<int*>(w + 128 + kArgmaxBlocks * sizeof(float));
+    const int blocks = n < kArgmaxBlocks * 256 ? (n + 255) / 256 : kArgmaxBlocks;
+    return (int)launch_pdl(argmax_kernel, dim3(blocks), dim3(256), st, static_cast<const __half*>(x), n, out, bv, bi,
+                           cnt);
+}
+
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st) {
     return (int)launch_pdl(silu_mul_kernel, dim3((n + 255) / 256), dim3(256), st, static_cast<const __half*>(g),
                            static_cast<const __half*>(u), static_cast<__half*>(a), n);

@@ -59,6 +59,8 @@ int launch_rope_attn_decode(const void* q, const void* k, const void* v, const f
 int launch_attn_decode(const void* q, const void* kc, const void* vc, int heads, int kv_heads, int lmax, int L,
                        float scale, void* out, void* ws, cudaStream_t st);
 int launch_silu_mul(const void* g, const void* u, void* a, int n, cudaStream_t st);
+size_t argmax_workspace_bytes();
+int launch_argmax(const void* x, int n, long long* out, void* ws, cudaStream_t st);
 
 // BCQ fitting (abcq_quantize.cu), f64, codes int8 (q, rows, cols)
 int launch_fit_greedy(const double* w, int rows, int cols, int g, int q, int asym, int8_t* codes, double* alpha,

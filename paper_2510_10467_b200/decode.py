@@ -78,6 +78,21 @@ def silu_mul(g, u, a):
                "abcq_silu_mul_f16")
 
 
+class _Argmax:
+    """Greedy token: abcq_argmax_f16 over the logits (one PDL launch; torch.argmax
+    took ~40 us on 128K logits) into a preallocated int64 scalar."""
+
+    def __init__(self, device):
+        n = C.c_size_t()
+        _lib.check(_lib.lib().abcq_argmax_workspace_bytes(C.byref(n)))
+        self.ws = torch.zeros(int(n.value), dtype=torch.uint8, device=device)
+
+    def __call__(self, logits, out):
+        _lib.check(_lib.lib().abcq_argmax_f16(logits.data_ptr(), logits.numel(), out.data_ptr(), self.ws.data_ptr(),
+                                              self.ws.numel(), _stream()), "abcq_argmax_f16")
+        return out
+
+
 def _rope_tables(cfg: LlamaConfig, pos: int, device):
     d = cfg.head_dim
     inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=device, dtype=torch.float64) / d))
@@ -172,6 +187,8 @@ class QuantizedLlamaStep:
         self.d = torch.empty(hd, **f16)
         self.h, self.act = torch.empty(hd, **f16), torch.empty(inter, **f16)
         self.token = torch.empty((), device=self.device, dtype=torch.int64)
+        self.logits = torch.empty(cfg.vocab, **f16)
+        self.argmax = _Argmax(self.device)
 
     def linear_bytes(self) -> int:
         """Algorithmic bytes the quantized linears read per step (planes + set p)."""
@@ -206,8 +223,8 @@ class QuantizedLlamaStep:
                 mats["down"].gemv(p, self.act, out=self.d)
             resid = self.d
         add_rmsnorm(self.x, resid, self.final_norm, self.h, cfg.eps)
-        torch.argmax(torch.mv(self.lm_head, self.h), out=self.token)
-        return self.token
+        torch.mv(self.lm_head, self.h, out=self.logits)
+        return self.argmax(self.logits, self.token)
 
 
 class Fp16LlamaStep:
@@ -236,6 +253,8 @@ class Fp16LlamaStep:
         self.qkv, self.gu = torch.empty(hd + 2 * kvd, **f16), torch.empty(2 * inter, **f16)
         self.act = torch.empty(inter, **f16)
         self.token = torch.empty((), device=self.device, dtype=torch.int64)
+        self.logits = torch.empty(cfg.vocab, **f16)
+        self.argmax = _Argmax(self.device)
 
     def linear_bytes(self) -> int:
         return sum(r * c * 2 for _, r, c in self.cfg.linear_shapes()) * self.cfg.layers
@@ -255,8 +274,8 @@ class Fp16LlamaStep:
             torch.mv(w["down"], self.act, out=self.d)
             resid = self.d
         add_rmsnorm(self.x, resid, self.norm_w, self.h, cfg.eps)
-        torch.argmax(torch.mv(self.lm_head, self.h), out=self.token)
-        return self.token
+        torch.mv(self.lm_head, self.h, out=self.logits)
+        return self.argmax(self.logits, self.token)
 
 
 def time_step(model, iters: int = 20, warmup: int = 3) -> float:

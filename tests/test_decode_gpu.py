@@ -207,3 +207,17 @@ def test_quantized_step_matches_dense_dequantized_step(p):
     rel = lambda a, b: float((a - b).norm() / b.norm())  # noqa: E731
     assert rel(x_q, x_d) <= 1e-2, rel(x_q, x_d)
     assert rel(h_q, h_d) <= 1e-2, rel(h_q, h_d)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 128256, 40000])
+def test_argmax_matches_torch(n):
+    from paper_2510_10467_b200.decode import _Argmax
+    am = _Argmax(torch.device("cuda"))
+    g = torch.Generator(device="cuda").manual_seed(n)
+    out = torch.empty((), device="cuda", dtype=torch.int64)
+    for trial in range(3):
+        x = torch.randn(n, device="cuda", generator=g).half()
+        if trial == 2 and n > 10:   # ties: the first occurrence wins
+            x[n // 3] = x[n - 2] = x.max() + 1
+        am(x, out)
+        assert int(out) == int(torch.argmax(x)), (n, trial)

@@ -149,6 +149,17 @@ int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
               int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ---- GEMV with a fused add + RMSNorm input (decoder step) -----------------
+ * y = W_p * h, h = f16(f16(x + residual) * rsqrt(mean(f16(x + residual)^2)
+ * + eps) * norm_w) -- exactly abcq_add_rmsnorm_f16's output (bitwise), formed
+ * by every CTA of the persistent kernel while it builds its tables (one
+ * launch instead of two); x + residual is written to d_x_out (if not NULL;
+ * must not alias d_x / d_residual). f16 x / residual / norm_w / x_out,
+ * cols <= 8192, TILED layout; workspace as abcq_gemv.                       */
+int abcq_gemv_add_rmsnorm(const abcq_model_t* m, int32_t p, const void* d_x, const void* d_residual,
+                          const void* d_norm_w, float eps, void* d_x_out, void* d_y, int32_t y_dtype,
+                          void* d_workspace, size_t workspace_bytes, void* stream);
+
 /* ---- batches of independent GEMVs ----------------------------------------
  * One persistent launch runs n_jobs GemvEngine.lut calls back to back (the
  * TMA stream never drains between them) -- e.g. q/k/v or gate/up of a

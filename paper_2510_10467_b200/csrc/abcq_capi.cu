@@ -201,6 +201,23 @@ int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype
                     "abcq_gemv");
 }
 
+int abcq_gemv_add_rmsnorm(const abcq_model_t* m, int32_t p, const void* d_x, const void* d_residual,
+                          const void* d_norm_w, float eps, void* d_x_out, void* d_y, int32_t y_dtype,
+                          void* d_workspace, size_t workspace_bytes, void* stream) {
+    if (int rc = check_call(m, p, d_x, ABCQ_F16, d_y, y_dtype)) return rc;
+    if (!abcq::lut_supports(m, p)) return fail(ABCQ_E_LAYOUT, "abcq_gemv_add_rmsnorm needs the tiled layout (group 128)");
+    if (!d_norm_w) return fail(ABCQ_E_ARG, "abcq_gemv_add_rmsnorm: norm weight is NULL");
+    if (m->cols > abcq::kRmsMaxN) return fail(ABCQ_E_ARG, "abcq_gemv_add_rmsnorm: cols %d > %d", m->cols, abcq::kRmsMaxN);
+    if (d_x_out && (d_x_out == d_x || d_x_out == d_residual))
+        return fail(ABCQ_E_ARG, "abcq_gemv_add_rmsnorm: x_out must not alias x or residual (every CTA reads them)");
+    const size_t need = abcq::lut_workspace_bytes(m);
+    if (need && (!d_workspace || workspace_bytes < need))
+        return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+    abcq::NormIn nin{d_x, d_residual, d_norm_w, d_x_out, eps};
+    return cuda_ret(abcq::launch_gemv_add_rmsnorm(m, p, nin, d_y, y_dtype, d_workspace, (cudaStream_t)stream),
+                    "abcq_gemv_add_rmsnorm");
+}
+
 int abcq_gemv_batch_max_jobs(void) { return abcq::lut_max_jobs(); }
 
 static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {

@@ -216,3 +216,54 @@ __device__ __forceinline__ void prefetch_l2_range(const void* src, int64_t bytes
     }
 }
 }  // namespace abcq
+
+namespace abcq {
+// ---------------------------------------------------------------------------
+// add + RMSNorm statistics shared bitwise by add_rmsnorm_kernel and the GEMV's
+// fused input mode (ABCQ add_rmsnorm GEMV): a 512-thread block; thread t owns
+// elements 8t..8t+7 and 4096+8t..4096+8t+7 (n <= 8192); v = f16(x + r) (the
+// residual stream is kept in f16); ss summed per thread in element order, then
+// an xor-butterfly per warp, then the 16 warp sums in warp order.
+// ---------------------------------------------------------------------------
+constexpr int kRmsThreads = 512;
+constexpr int kRmsMaxN = 8192;
+
+__device__ __forceinline__ float rms_warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// v[16] = f16(x + r) of the thread's elements (0 beyond n); returns the
+// thread's partial sum of squares
+__device__ __forceinline__ float rms_load(const __half* x, const __half* r, int n, int t, float (&v)[16]) {
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int i = (k < 8 ? 8 * t + k : 4096 + 8 * t + (k - 8));
+        float xv = 0.f;
+        if (i < n) {
+            xv = __half2float(x[i]);
+            if (r) xv = __half2float(__float2half_rn(xv + __half2float(r[i])));
+        }
+        v[k] = xv;
+        ss += xv * xv;
+    }
+    return ss;
+}
+
+// block-wide inverse RMS (all 512 threads call; red: 17 floats of shared memory)
+__device__ __forceinline__ float rms_inv(float ss, int n, float eps, float* red) {
+    ss = rms_warp_sum(ss);
+    const int t = threadIdx.x;
+    if ((t & 31) == 0) red[t >> 5] = ss;
+    __syncthreads();
+    if (t == 0) {
+        float tot = 0.f;
+        for (int w = 0; w < kRmsThreads / 32; ++w) tot += red[w];
+        red[16] = rsqrtf(tot / n + eps);
+    }
+    __syncthreads();
+    return red[16];
+}
+}  // namespace abcq

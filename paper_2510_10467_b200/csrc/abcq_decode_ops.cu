@@ -49,40 +49,23 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // one block of 1024 threads; n <= 8192 (4 values per thread, half2 loads)
-__global__ void __launch_bounds__(1024) add_rmsnorm_kernel(__half* __restrict__ x, const __half* __restrict__ r,
-                                                           const __half* __restrict__ w, __half* __restrict__ y,
-                                                           int n, float eps) {
+__global__ void __launch_bounds__(kRmsThreads) add_rmsnorm_kernel(__half* __restrict__ x,
+                                                                  const __half* __restrict__ r,
+                                                                  const __half* __restrict__ w,
+                                                                  __half* __restrict__ y, int n, float eps) {
     pdl_enter();
-    __shared__ float red[32];
-    float v[8];
-    float ss = 0.f;
+    __shared__ float red[17];
+    float v[16];
+    const int t = threadIdx.x;
+    const float ss = rms_load(x, r, n, t, v);  // (the statistics the fused GEMV input recomputes bitwise)
+    const float inv = rms_inv(ss, n, eps, red);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 1024;
-        float xv = 0.f;
+    for (int k = 0; k < 16; ++k) {
+        const int i = (k < 8 ? 8 * t + k : 4096 + 8 * t + (k - 8));
         if (i < n) {
-            xv = __half2float(x[i]);
-            if (r) {
-                xv = __half2float(__float2half_rn(xv + __half2float(r[i])));  // residual stream kept in f16
-                x[i] = __float2half_rn(xv);
-            }
+            if (r) x[i] = __float2half_rn(v[k]);
+            y[i] = __float2half_rn(v[k] * inv * __half2float(w[i]));
         }
-        v[k] = xv;
-        ss += xv * xv;
-    }
-    ss = warp_sum(ss);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float t = warp_sum(red[threadIdx.x]);
-        if (threadIdx.x == 0) red[0] = rsqrtf(t / n + eps);
-    }
-    __syncthreads();
-    const float inv = red[0];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = threadIdx.x + k * 1024;
-        if (i < n) y[i] = __float2half_rn(v[k] * inv * __half2float(w[i]));
     }
 }
 
@@ -347,7 +330,7 @@ __global__ void silu_mul_kernel(const __half* __restrict__ g, const __half* __re
 }
 
 int launch_add_rmsnorm(void* x, const void* r, const void* w, void* y, int n, float eps, cudaStream_t st) {
-    return (int)launch_pdl(add_rmsnorm_kernel, dim3(1), dim3(1024), st, static_cast<__half*>(x),
+    return (int)launch_pdl(add_rmsnorm_kernel, dim3(1), dim3(kRmsThreads), st, static_cast<__half*>(x),
                            static_cast<const __half*>(r), static_cast<const __half*>(w), static_cast<__half*>(y), n,
                            eps);
 }

@@ -36,6 +36,11 @@ struct Job {
     float* partial;      // [NRT][NS][16]: a row tile's slice partials are one contiguous run
     int rows, cols, NRT, NS, p, items;
     int glu;        // x = [g ; u] (2*cols f16): input f16(silu(g) * u) (ABCQ_F16_SILU_GLU)
+    int nrm;        // input f16(f16(x + res) * inv_rms * nw) (abcq_gemv_add_rmsnorm; single-job launches)
+    const __half* res;  // residual added to x (may be NULL)
+    const __half* nw;   // RMSNorm weight
+    __half* xo;         // x + res written back (the residual stream; may be NULL)
+    float eps;
     uint32_t* arrive;   // CTAs done streaming this job (split jobs; self-resetting)
     uint32_t* reduced;  // reduce blocks done with this job (self-resetting)
     int ncta;           // CTAs whose range touches this job
@@ -497,9 +502,29 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         for (int h = 0; h < 16; ++h) col[(u + 16 * h) * 64] = ev[h];
         if (ASYM && u == 15) csum[half_sel * 32 + c] = ev[15];  // T[255] = chunk sum
     };
+    float* nrm_red = reinterpret_cast<float*>(smem + 800);  // [17]: RMSNorm statistics (norm input mode)
+    auto load_job_x8 = [&](const Job& Jn, int k0, float (&xv)[8]) {
+        if (Jn.nrm) {  // f16(f16(x + res) * inv * w): add_rmsnorm_kernel's expression, bitwise
+            const float inv = nrm_red[16];
+            const __half* xh = static_cast<const __half*>(Jn.x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = k0 + j;
+                float v = 0.f;
+                if (i < Jn.cols) {
+                    v = __half2float(xh[i]);
+                    if (Jn.res) v = __half2float(__float2half_rn(v + __half2float(Jn.res[i])));
+                    v = __half2float(__float2half_rn(v * inv * __half2float(Jn.nw[i])));
+                }
+                xv[j] = v;
+            }
+        } else {
+            load_x8_any<XT>(static_cast<const XT*>(Jn.x), k0, Jn.cols, Jn.glu, xv);
+        }
+    };
     auto piece_x = [&](const Round& Rn, int c, float (&xv)[8]) {
         const Job& Jn = a.jobs[Rn.pc[0].j];
-        load_x8_any<XT>(static_cast<const XT*>(Jn.x), Rn.pc[0].s * kSliceCols + 8 * c, Jn.cols, Jn.glu, xv);
+        load_job_x8(Jn, Rn.pc[0].s * kSliceCols + 8 * c, xv);
     };
 
     int e = 0;  // consumed elements (slot = e % R, phase = (e / R) & 1)
@@ -507,10 +532,29 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     pdl_wait();  // x, y and the workspace belong to the previous kernel
     pdl_launch_dependents();
     if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
+    if (a.jobs[0].nrm) {  // RMSNorm statistics of the whole input (every CTA, bitwise as add_rmsnorm)
+        const Job& J = a.jobs[0];
+        float v[16];
+        const float ss = rms_load(static_cast<const __half*>(J.x), J.res, J.cols, tid, v);
+        rms_inv(ss, J.cols, J.eps, nrm_red);
+        if (J.xo && blockIdx.x == 0) {  // the updated residual stream (one CTA writes it)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int i = (k < 8 ? 8 * tid + k : 4096 + 8 * tid + (k - 8));
+                if (i < J.cols) J.xo[i] = __float2half_rn(v[k]);
+            }
+        }
+    }
     {
         float xv0[8], xv1[8];
-        if (has0) load_x8_any<XT>(xp0, xk0, xc0, xg0, xv0);
-        if (has1) load_x8_any<XT>(xp1, xk1, xc1, xg1, xv1);
+        if (has0) {
+            if (a.jobs[R0.pc[0].j].nrm) load_job_x8(a.jobs[R0.pc[0].j], xk0, xv0);
+            else load_x8_any<XT>(xp0, xk0, xc0, xg0, xv0);
+        }
+        if (has1) {
+            if (a.jobs[R1.pc[0].j].nrm) load_job_x8(a.jobs[R1.pc[0].j], xk1, xv1);
+            else load_x8_any<XT>(xp1, xk1, xc1, xg1, xv1);
+        }
         for (; s_fill < R && ic.rs < it1; ++s_fill) {  // rest of the ring, behind x
             issue(ic, s_fill);
             advance(ic);

@@ -59,6 +59,11 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.offset = m->asymmetric ? m->offset[p] : nullptr;
     J.x = x;
     J.glu = 0;
+    J.nrm = 0;
+    J.res = nullptr;
+    J.nw = nullptr;
+    J.xo = nullptr;
+    J.eps = 0.f;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
     J.ncta = 0;
@@ -71,7 +76,7 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 }
 
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st) {
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin) {
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
     // fixed cost of a (job, slice) piece in blocks: measured best 300 for
@@ -87,6 +92,13 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     for (int j = 0; j < n; ++j) {
         make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
         a.jobs[j].glu = x_dtypes[j] == ABCQ_F16_SILU_GLU;
+        if (nin && j == 0) {
+            a.jobs[0].nrm = 1;
+            a.jobs[0].res = static_cast<const __half*>(nin->residual);
+            a.jobs[0].nw = static_cast<const __half*>(nin->norm_w);
+            a.jobs[0].xo = static_cast<__half*>(nin->x_out);
+            a.jobs[0].eps = nin->eps;
+        }
         w += partial_bytes(models[j]);
         a.jobs[j].arrive = counters ? counters + j * kCounterStride : nullptr;
         a.jobs[j].reduced = counters ? counters + (kMaxJobs + j) * kCounterStride : nullptr;
@@ -207,6 +219,13 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
 int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, int y_dtype,
                     void* ws, cudaStream_t st) {
     return launch_gemv_jobs(&m, &p, &x, &y, 1, &x_dtype, y_dtype, ws, st);
+}
+
+int launch_gemv_add_rmsnorm(const abcq_model_t* m, int p, const NormIn& nin, void* y, int y_dtype, void* ws,
+                            cudaStream_t st) {
+    const int xd = ABCQ_F16;
+    const void* x = nin.x;
+    return launch_gemv_jobs(&m, &p, &x, &y, 1, &xd, y_dtype, ws, st, &nin);
 }
 
 }  // namespace abcq

@@ -25,9 +25,22 @@ int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, vo
                     void* ws, cudaStream_t st);
 // batch of n independent GEMVs (same dtypes / mode), workspaces concatenated
 // in job order (lut_workspace_bytes each)
+struct NormIn;
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st);
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin = nullptr);
 int lut_max_jobs();
+
+// fused input mode of the persistent GEMV: input = f16(f16(x + residual) * inv_rms * norm_w),
+// x + residual written to x_out (add_rmsnorm_kernel's arithmetic, bitwise)
+struct NormIn {
+    const void* x;
+    const void* residual;
+    const void* norm_w;
+    void* x_out;
+    float eps;
+};
+int launch_gemv_add_rmsnorm(const abcq_model_t* m, int p, const NormIn& nin, void* y, int y_dtype, void* ws,
+                            cudaStream_t st);
 
 // single GEMV through the cluster kernel (abcq_gemv_cluster.cu): no workspace
 bool cluster_supports(const abcq_model_t* m, int p);

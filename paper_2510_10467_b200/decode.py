@@ -149,8 +149,15 @@ class QuantizedLlamaStep:
     """Decode step with AnyBCQ linears at precision p (p_lo..p_hi resident)."""
 
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), p: int = 3, p_lo: int = 2, p_hi: int = 4,
-                 ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True, stack_rows: bool = True):
+                 ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True, stack_rows: bool = True,
+                 fuse_norm: bool = False):
         self.cfg, self.p, self.fuse_glu, self.stack_rows = cfg, p, fuse_glu, stack_rows
+        # fuse_norm: add + RMSNorm formed inside the q/k/v and gate/up GEMVs'
+        # table builds (abcq_gemv_add_rmsnorm, bitwise equal to the separate
+        # launch). Off by default: measured 2.14 vs 2.11 ms/token at p=3 -- every
+        # CTA then waits for the whole-vector statistics before its tables,
+        # while the separate launch overlaps the GEMV's weight prefetch (PDL)
+        self.fuse_norm = fuse_norm
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.layers = []
@@ -179,6 +186,7 @@ class QuantizedLlamaStep:
         hd, kvd, inter = cfg.hidden, cfg.kv_heads * cfg.head_dim, cfg.intermediate
         f16 = dict(device=self.device, dtype=torch.float16)
         self.x = torch.randn(hd, **f16, generator=gen)
+        self.x_alt = torch.empty(hd, **f16)  # the fused norms write x + residual here (ping-pong)
         self.qkv = torch.empty(hd + 2 * kvd, **f16)
         self.q, self.k, self.v = self.qkv[:hd], self.qkv[hd:hd + kvd], self.qkv[hd + kvd:]
         self.o = torch.empty(hd, **f16)
@@ -195,33 +203,47 @@ class QuantizedLlamaStep:
         p = self.p
         return sum(p * r * c // 8 + p * r * (c // 128) * 2 for _, r, c in self.cfg.linear_shapes()) * self.cfg.layers
 
+    def _norm_linear(self, mats, name, cur, nxt, resid, w, out):
+        """out = W rmsnorm(cur + resid) * w; returns the residual stream buffer
+        after the add (nxt when the norm is fused into the GEMV, else cur)."""
+        cfg, p = self.cfg, self.p
+        dm = mats.get(name)
+        if self.fuse_norm and self.stack_rows and isinstance(dm, DeviceModel):
+            dm.gemv_add_rmsnorm(p, cur, resid, w, cfg.eps, out=out, x_out=nxt)
+            return nxt
+        add_rmsnorm(cur, resid, w, self.h, cfg.eps)
+        if self.stack_rows:
+            _persistent(dm, p, self.h, out) if name == "qkv" else dm.gemv(p, self.h, out=out)
+        elif name == "qkv":
+            gemv_batch([(mats["q"], p, self.h, self.q), (mats["k"], p, self.h, self.k),
+                        (mats["v"], p, self.h, self.v)])
+        else:
+            gemv_batch([(mats["gate"], p, self.h, self.g), (mats["up"], p, self.h, self.u)])
+        return cur
+
     def step(self):
         cfg, p = self.cfg, self.p
         resid = None
+        cur, nxt = self.x, self.x_alt  # an even number of fused norms per step: it ends in self.x
         for li, mats in enumerate(self.layers):
-            add_rmsnorm(self.x, resid, self.norm_w[li][0], self.h, cfg.eps)
             # q/k/v and o through the persistent batch kernel even as single jobs:
             # between the step's other kernels it measured faster than the
             # latency-path cluster kernel abcq_gemv takes for these shapes
             # (p3: 2.19 vs 2.25 ms/token, tools/decode_ab.py; DESIGN §3.1b)
-            if self.stack_rows:
-                _persistent(mats["qkv"], p, self.h, self.qkv)
-            else:
-                gemv_batch([(mats["q"], p, self.h, self.q), (mats["k"], p, self.h, self.k),
-                            (mats["v"], p, self.h, self.v)])
+            new = self._norm_linear(mats, "qkv", cur, nxt, resid, self.norm_w[li][0], self.qkv)
+            cur, nxt = (new, cur) if new is not cur else (cur, nxt)
             a = self.attn(li, self.q, self.k, self.v)
             _persistent(mats["o"], p, a, self.o)
-            add_rmsnorm(self.x, self.o, self.norm_w[li][1], self.h, cfg.eps)
-            if self.stack_rows:  # y = [gate ; up]: exactly the down GEMV's SiLU-gated input layout
-                mats["gu"].gemv(p, self.h, out=self.gu)
-            else:
-                gemv_batch([(mats["gate"], p, self.h, self.g), (mats["up"], p, self.h, self.u)])
+            # y = [gate ; up]: exactly the down GEMV's SiLU-gated input layout
+            new = self._norm_linear(mats, "gu", cur, nxt, self.o, self.norm_w[li][1], self.gu)
+            cur, nxt = (new, cur) if new is not cur else (cur, nxt)
             if self.fuse_glu:  # silu(gate)*up formed inside the down GEMV's table build
                 mats["down"].gemv(p, self.gu, out=self.d, silu_glu=True)
             else:
                 silu_mul(self.g, self.u, self.act)
                 mats["down"].gemv(p, self.act, out=self.d)
             resid = self.d
+        assert cur is self.x
         add_rmsnorm(self.x, resid, self.final_norm, self.h, cfg.eps)
         torch.mv(self.lm_head, self.h, out=self.logits)
         return self.argmax(self.logits, self.token)

@@ -268,6 +268,23 @@ class DeviceModel:
             out.data_ptr(), dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv")
         return out
 
+    def gemv_add_rmsnorm(self, p: int, x: torch.Tensor, residual, norm_w: torch.Tensor, eps: float,
+                         out: torch.Tensor, x_out=None, stream=None) -> torch.Tensor:
+        """out = W_p rmsnorm(x + residual) * norm_w, one persistent launch (the
+        decoder's add+RMSNorm fused into the GEMV input; abcq_gemv_add_rmsnorm).
+        x, residual, norm_w, x_out: f16 (cols,) CUDA tensors; x_out receives x + residual."""
+        self._check_p(p)
+        for t in (x, norm_w) + ((residual,) if residual is not None else ()) + ((x_out,) if x_out is not None else ()):
+            if t.dtype != torch.float16 or t.numel() != self.cols or t.device != self.device or not t.is_contiguous():
+                raise UsageError("x / residual / norm_w / x_out must be contiguous f16 tensors of `cols` elements")
+        self._order_after_upload(p, stream)
+        ws = self.workspace(stream)
+        _lib.check(_lib.lib().abcq_gemv_add_rmsnorm(
+            self.struct_ptr(), p, x.data_ptr(), _lib.ptr(residual), norm_w.data_ptr(), float(eps), _lib.ptr(x_out),
+            out.data_ptr(), dtype_code(out.dtype), ws.data_ptr(), ws.numel(), _stream_handle(stream)),
+            "abcq_gemv_add_rmsnorm")
+        return out
+
     def gemm_mixedp(self, ps, X: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
         """Y[b] = W_{ps[b]} X[b] for B <= 16 requests in one pass over the planes
         (tensor cores). X: (B, cols) CUDA tensor (cast to fp16); returns (B, rows)."""

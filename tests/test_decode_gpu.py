@@ -221,3 +221,50 @@ def test_argmax_matches_torch(n):
             x[n // 3] = x[n - 2] = x.max() + 1
         am(x, out)
         assert int(out) == int(torch.argmax(x)), (n, trial)
+
+
+def test_quantized_step_fused_norm_equals_separate_add_rmsnorm():
+    """add + RMSNorm inside the q/k/v and gate/up GEMVs (abcq_gemv_add_rmsnorm)
+    == the separate add_rmsnorm launch: bitwise equal step state and token."""
+    from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    cfg = LlamaConfig(layers=3, vocab=1000)
+    m = QuantizedLlamaStep(cfg, p=3, ctx=64, fuse_norm=True)
+    x0 = m.x.clone()
+    k0, v0 = m.attn.k_cache.clone(), m.attn.v_cache.clone()
+    t1 = m.step().item()
+    x1, gu1, qkv1 = m.x.clone(), m.gu.clone(), m.qkv.clone()
+    m.x.copy_(x0)
+    m.attn.k_cache.copy_(k0)
+    m.attn.v_cache.copy_(v0)
+    m.fuse_norm = False
+    t2 = m.step().item()
+    assert t1 == t2
+    assert torch.equal(m.x, x1) and torch.equal(m.gu, gu1) and torch.equal(m.qkv, qkv1)
+
+
+def test_gemv_add_rmsnorm_matches_separate_ops():
+    """One model, the fused input vs add_rmsnorm + gemv (both bitwise), incl.
+    no residual, and the C-ABI alias check."""
+    import paper_2510_10467_b200 as P
+    from paper_2510_10467_b200.decode import add_rmsnorm
+    dm = P.DeviceModel(6144, 4096, 128, 2, 4, scale_dtype="f16")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, 6144, 128), dtype=torch.int32, device="cuda", generator=g))
+    for q in (2, 3, 4):
+        dm.load_scale_set(q, 0.01 + 0.01 * torch.rand((q, 6144, 32), device="cuda", generator=g))
+    x = torch.randn(4096, device="cuda", generator=g).half()
+    r = torch.randn(4096, device="cuda", generator=g).half()
+    w = (1 + 0.1 * torch.randn(4096, device="cuda", generator=g)).half()
+    for res in (r, None):
+        xo = torch.empty_like(x)
+        y = torch.empty(6144, device="cuda", dtype=torch.float16)
+        dm.gemv_add_rmsnorm(3, x, res, w, 1e-5, out=y, x_out=xo)
+        xs, h = x.clone(), torch.empty_like(x)
+        add_rmsnorm(xs, res, w, h, 1e-5)
+        want = torch.empty_like(y)
+        P.gemv_batch([(dm, 3, h, want)])
+        torch.cuda.synchronize()
+        assert torch.equal(y, want)
+        assert torch.equal(xo, xs)
+    with pytest.raises(P.UsageError):
+        dm.gemv_add_rmsnorm(3, x, r, w, 1e-5, out=y, x_out=x)   # x_out aliases x

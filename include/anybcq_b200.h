@@ -96,12 +96,13 @@ int abcq_debug_set_trace(void* d_buf);
  * skip the table lookups, 2 = skip the weight loads; 23 = route single GEMVs
  * through the batch kernel instead of the cluster kernel; 27 = route every
  * single GEMV through the cluster kernel; 5000 + 100*slots + 10*C + t = force
- * the cluster kernel's geometry (C digit 6 = 16; 5000 = automatic). Default 0. */
+ * the cluster kernel's geometry (C digit 6 = 16; 5000 = automatic); 6000 + W =
+ * force its consumer warps (8 / 16; 6000 = automatic). Default 0. */
 int abcq_debug_set_mode(int32_t mode);
 /* profiling aid: the launch geometry a single GEMV (abcq_gemv, or a batch of
  * one job) uses for this model and precision -- out7 = {cluster size C,
- * clusters M, CTAs per SM, tiles per stage, ring slots, stage bytes, dynamic
- * shared-memory bytes}; ABCQ_E_LAYOUT when the call takes another kernel.  */
+ * clusters M, CTAs per SM, tiles per stage, ring slots, consumer warps,
+ * dynamic shared-memory bytes}; ABCQ_E_LAYOUT when the call takes another kernel. */
 int abcq_debug_gemv_geometry(const abcq_model_t* m, int32_t p, int32_t* out7);
 
 /* ---- layout sizes (host-only arithmetic) ---------------------------------
@@ -140,7 +141,7 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
  * x: (cols) in x_dtype, 16-byte aligned (TILED); y: (rows) in y_dtype.
  * TILED layout -> an sm_100a LUT kernel: the cluster kernel (split-K through
  * distributed shared memory, one launch, no workspace use) for latency-bound
- * GEMVs (<= 16 MiB of planes and <= 32 column slices), else the persistent
+ * GEMVs (<= 24 MiB of planes and <= 32 column slices), else the persistent
  * streaming kernel; ROWMAJOR layout (any group size) -> the generic kernel.
  * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials + self-
  * resetting completion counters): zero-filled once before first use; may

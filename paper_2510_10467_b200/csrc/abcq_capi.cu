@@ -77,6 +77,10 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
+    if (mode >= 6000 && mode < 6100) {  // cluster GEMV consumer warps: 6000 + W (8 / 16; 6000 = automatic)
+        abcq::g_cl_warps = mode - 6000;
+        return 0;
+    }
     if (mode >= 5000 && mode < 6000) {  // cluster GEMV geometry: 5000 + 100*slots + 10*C + tiles/warp (5000 = auto; C digit 6 = 16)
         abcq::g_cl_force = mode - 5000;
         return 0;

@@ -7,6 +7,7 @@
 namespace abcq {
 
 int g_cl_force = 0;  // abcq_debug_set_mode(5000 + 100*slots + 10*C + tcw): forced geometry (0 = automatic)
+int g_cl_warps = 0;  // abcq_debug_set_mode(6000 + W): consumer warps per CTA (0 = automatic)
 
 namespace cl {
 
@@ -23,12 +24,12 @@ static int max_clusters(int C) {
     if (C == 1) {
         n = num_sms();
     } else {
-        auto kern = gemv_cluster_kernel<__half, __half, __half, false>;
+        auto kern = gemv_cluster_kernel<__half, __half, __half, false, 16>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem1);
         if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C * 64);
-        cfg.blockDim = dim3(kThreads);
+        cfg.blockDim = dim3(threads_of<16>());
         cfg.dynamicSmemBytes = kSmem1;  // one CTA per SM: the clusters one grid can spread over
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -47,7 +48,7 @@ static int max_clusters(int C) {
 }
 
 struct Geom {
-    int C, M, slots, tc, ring, stage_bytes, part_off, xs_off, recv_off, ring_off, smem;
+    int C, M, slots, tc, ring, stage_bytes, part_off, xs_off, recv_off, ring_off, smem, W;
 };
 
 static bool plan(const abcq_model_t* m, int p, Geom& g) {
@@ -90,21 +91,27 @@ static bool plan(const abcq_model_t* m, int p, Geom& g) {
     const int recv_bytes = bc > 1 ? (Tm * 16 + 8) * 4 : 0;
     const int ring_off = (recv_off + recv_bytes + 127) / 128 * 128;
     // stage = (slice, chunk of tc tiles, all p planes); one or two tiles per consumer warp
-    int tcw = forced_tcw ? forced_tcw : 2;
+    // consumer warps: 8 when two CTAs share an SM (register budget); alone, 16
+    // for bands of >= 48 tiles up to p = 3, else 8 (16 warps x 2 tiles x p >= 4
+    // planes make stages too large for a ring deeper than 2, and short bands
+    // leave warps idle; tools/cl_probe.py)
+    const int W = g_cl_warps ? g_cl_warps : (slots == 2 || p > 3 || Tm < 48 ? 8 : 16);
+    int tcw = forced_tcw ? forced_tcw : kMaxTCW;
     if (tcw > kMaxTCW) tcw = kMaxTCW;
-    const int nch = (int)ceil_div(Tm, kW * tcw);
+    const int nch = (int)ceil_div(Tm, W * tcw);
     const int tc = (int)ceil_div(Tm, nch);
     const int stage = (p * tc * (kBlockBytes + 32 * esz) + (zmul - 1) * tc * 32 * esz + 127) / 128 * 128;
     int ring = (smem - ring_off) / stage;
     if (ring > kMaxRing) ring = kMaxRing;
     if (ring < 1) return false;
-    g = Geom{bc, bm, slots, tc, ring, stage, part_off, xs_off, recv_off, ring_off, ring_off + ring * stage};
+    if (slots == 2 && W != 8) return false;
+    g = Geom{bc, bm, slots, tc, ring, stage, part_off, xs_off, recv_off, ring_off, ring_off + ring * stage, W};
     return true;
 }
 
-template <typename XT, typename YT, typename ST, bool ASYM>
+template <typename XT, typename YT, typename ST, bool ASYM, int W>
 static int launch_t(const Args& a, int smem, cudaStream_t st) {
-    auto kern = gemv_cluster_kernel<XT, YT, ST, ASYM>;
+    auto kern = gemv_cluster_kernel<XT, YT, ST, ASYM, W>;
     static bool attr_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -119,7 +126,7 @@ static int launch_t(const Args& a, int smem, cudaStream_t st) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.M * a.C);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads_of<W>());
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -139,11 +146,16 @@ static int launch_t(const Args& a, int smem, cudaStream_t st) {
     return (int)cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <typename XT, typename YT>
-static int launch_xy(const Args& a, int sd, bool asym, int smem, cudaStream_t st) {
+template <typename XT, typename YT, int W>
+static int launch_w(const Args& a, int sd, bool asym, int smem, cudaStream_t st) {
     if (sd == ABCQ_F16)
-        return asym ? launch_t<XT, YT, __half, true>(a, smem, st) : launch_t<XT, YT, __half, false>(a, smem, st);
-    return asym ? launch_t<XT, YT, float, true>(a, smem, st) : launch_t<XT, YT, float, false>(a, smem, st);
+        return asym ? launch_t<XT, YT, __half, true, W>(a, smem, st) : launch_t<XT, YT, __half, false, W>(a, smem, st);
+    return asym ? launch_t<XT, YT, float, true, W>(a, smem, st) : launch_t<XT, YT, float, false, W>(a, smem, st);
+}
+
+template <typename XT, typename YT>
+static int launch_xy(const Args& a, int sd, bool asym, int smem, int W, cudaStream_t st) {
+    return W == 16 ? launch_w<XT, YT, 16>(a, sd, asym, smem, st) : launch_w<XT, YT, 8>(a, sd, asym, smem, st);
 }
 
 }  // namespace cl
@@ -151,12 +163,12 @@ static int launch_xy(const Args& a, int sd, bool asym, int smem, cudaStream_t st
 bool cluster_supports(const abcq_model_t* m, int p) {
     if (m->layout != ABCQ_LAYOUT_TILED || p < 1 || p > ABCQ_MAX_PLANES || g_dbg_mode == 23) return false;
     // dispatch (tools/cl_probe.py, back-to-back single launches, B200): the
-    // cluster kernel wins while a GEMV is latency-bound -- up to ~16 MB of plane
+    // cluster kernel wins while a GEMV is latency-bound -- up to ~24 MB of plane
     // bytes and <= 2 slices per CTA at C = 16; larger GEMVs stream better
     // through the persistent batch kernel (more CTAs, deeper rings)
     if (g_dbg_mode != 27) {  // (27: every single GEMV through the cluster kernel -- test coverage)
         const int64_t plane_bytes = (int64_t)p * tiled_plane_bytes(m->rows, m->cols);
-        if (n_slices(m->cols) > 32 || plane_bytes > (int64_t)16 * 1024 * 1024) return false;
+        if (n_slices(m->cols) > 32 || plane_bytes > (int64_t)24 * 1024 * 1024) return false;
     }
     cl::Geom g;
     return cl::plan(m, p, g);
@@ -196,17 +208,17 @@ int launch_gemv_cluster(const abcq_model_t* m, int p, const void* x, int x_dtype
     const bool asym = m->asymmetric != 0;
     const int sd = m->scale_dtype;
     if (x_dtype == ABCQ_F32)
-        return y_dtype == ABCQ_F16 ? cl::launch_xy<float, __half>(a, sd, asym, g.smem, st)
-                                   : cl::launch_xy<float, float>(a, sd, asym, g.smem, st);
-    return y_dtype == ABCQ_F16 ? cl::launch_xy<__half, __half>(a, sd, asym, g.smem, st)
-                               : cl::launch_xy<__half, float>(a, sd, asym, g.smem, st);
+        return y_dtype == ABCQ_F16 ? cl::launch_xy<float, __half>(a, sd, asym, g.smem, g.W, st)
+                                   : cl::launch_xy<float, float>(a, sd, asym, g.smem, g.W, st);
+    return y_dtype == ABCQ_F16 ? cl::launch_xy<__half, __half>(a, sd, asym, g.smem, g.W, st)
+                               : cl::launch_xy<__half, float>(a, sd, asym, g.smem, g.W, st);
 }
 
-// geometry report for tools / tests: {C, M, slots, tc, ring, stage_bytes, smem}
+// geometry report for tools / tests: {C, M, slots, tc, ring, W (consumer warps), smem}
 int gemv_cluster_geometry(const abcq_model_t* m, int p, int* out7) {
     cl::Geom g;
     if (!cl::plan(m, p, g)) return -1;
-    const int v[7] = {g.C, g.M, g.slots, g.tc, g.ring, g.stage_bytes, g.smem};
+    const int v[7] = {g.C, g.M, g.slots, g.tc, g.ring, g.W, g.smem};
     for (int i = 0; i < 7; ++i) out7[i] = v[i];
     return 0;
 }

@@ -15,7 +15,8 @@
 // Per (plane, slice) a CTA's blocks are ONE contiguous byte range, so the
 // weights arrive by a handful of large TMA bulk copies.
 //
-// CTA = kW consumer warps + 1 producer warp:
+// CTA = W consumer warps (8 when two CTAs share an SM, 16 for one CTA per SM)
+// + 1 producer warp:
 //  * producer (one lane): streams stages (slice, tile chunk, plane) of weights,
 //    that plane's scales and (plane 0, asymmetric) offsets into a ring of
 //    shared-memory slots (cp.async.bulk ... mbarrier::complete_tx, full/empty
@@ -43,9 +44,9 @@
 namespace abcq {
 namespace cl {
 
-constexpr int kW = 8;                       // consumer warps
-constexpr int kThreads = (kW + 1) * 32;     // + one producer warp
 constexpr int kMaxTCW = 2;                  // tiles per consumer warp per stage
+template <int W>
+constexpr int threads_of() { return (W + 1) * 32; }  // W consumer warps + one producer warp
 constexpr int kMaxRing = 32;                // ring slots (barrier space)
 constexpr uint32_t kTBase = 0x800;          // table window address (low 16 bits)
 constexpr uint32_t kHdrBytes = 0x400;       // [dyn base, kTBase): barriers, chunk sums
@@ -63,7 +64,7 @@ struct Args {
     void* y;
     int rows, cols, NRT, NS, items, p, glu;
     int C, M;             // cluster size, clusters
-    int tc;               // max tiles per stage (<= kW * kMaxTCW)
+    int tc;               // max tiles per stage (<= W * kMaxTCW)
     int ring;             // ring slots
     int stage_bytes;      // bytes per slot
     int part_off;         // dynamic-smem offset of the [tile][16] partials
@@ -90,7 +91,8 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t local_addr, uint32_t rank
     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
     return v;
 }
-__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kW * 32) : "memory"); }
+template <int W>
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(W * 32) : "memory"); }
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
@@ -183,6 +185,38 @@ __device__ __forceinline__ void build_cols2(const float (&xa)[8], const float (&
     }
 }
 
+// the same build split over two threads (W = 16: 512 builders): entries
+// t = u + 16h for h in [8hb, 8hb + 8) -- the tree over x4..x6, then -/+ x7
+// (h bit 3 = hb): the reference's rounding sequence unchanged
+__device__ __forceinline__ void build_cols2_half(const float (&xa)[8], const float (&xb)[8], int u, int hb, int cp,
+                                                 uint32_t tbl_lo, int seg, uint32_t csum_lo) {
+    unsigned long long v = 0ull;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const unsigned long long xv = ((u >> j) & 1) ? pack2(xa[j], xb[j]) : pack2(-xa[j], -xb[j]);
+        v = fadd2(v, xv);
+    }
+    unsigned long long leaf[8];
+    leaf[0] = v;
+#pragma unroll
+    for (int j = 4; j < 7; ++j) {
+        const int n = 1 << (j - 4);
+        const unsigned long long px = pack2(xa[j], xb[j]), nx = pack2(-xa[j], -xb[j]);
+#pragma unroll
+        for (int k = n - 1; k >= 0; --k) {
+            leaf[k + n] = fadd2(leaf[k], px);
+            leaf[k] = fadd2(leaf[k], nx);
+        }
+    }
+    const unsigned long long x7 = hb ? pack2(xa[7], xb[7]) : pack2(-xa[7], -xb[7]);
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const float2 e = unpack2(fadd2(leaf[h], x7));
+        sts_v2(tbl_lo + (uint32_t)((u + 16 * (h + 8 * hb)) * 256 + seg * 128 + cp * 8), e.x, e.y);
+        if (h == 7 && hb && u == 15 && csum_lo) sts_v2(csum_lo + (uint32_t)((seg * 32 + 2 * cp) * 4), e.x, e.y);
+    }
+}
+
 // x values of chunk columns 2cp, 2cp+1 of slice s (16 consecutive inputs)
 template <typename XT>
 __device__ __forceinline__ void slice_x16(const Args& a, int s, int cp, float (&xa)[8], float (&xb)[8]) {
@@ -197,8 +231,8 @@ __device__ __forceinline__ void slice_x16(const Args& a, int s, int cp, float (&
         if (a.trace) a.trace[(size_t)blockIdx.x * 16 + (k)] = globaltimer();                   \
     } while (0)
 
-template <typename XT, typename YT, typename ST, bool ASYM>
-__global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_constant__ Args a) {
+template <typename XT, typename YT, typename ST, bool ASYM, int W>
+__global__ void __launch_bounds__(threads_of<W>(), (W == 8 ? 2 : 1)) gemv_cluster_kernel(const __grid_constant__ Args a) {
     extern __shared__ __align__(1024) char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t base = smem_addr(smem);
@@ -238,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         }
         for (int s = 0; s < R; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kW);
+            mbar_init(&empty[s], W);
         }
         fence_mbar_init();
     }
@@ -247,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
     // their rings while this grid runs (dbg 64: only once past the PDL wait)
     if (!(a.dbg & 64)) pdl_launch_dependents();
 
-    if (warp == kW) {
+    if (warp == W) {
         // ---------------- producer: weights/scales never depend on the previous kernel
         if (lane == 0 && nst > 0) {
             const uint64_t pol = l2_evict_first_policy();
@@ -295,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
             const uint32_t c1 = (uint32_t)((half * 16 + ((2 * k + 1 + r) & 15)) * 4);
             rb0[k] = c0 | (c1 << 8) | (tbl_lo & 0xFFFF0000u);
         }
-        for (int q = tid; q < T * 16; q += kW * 32) sts_f32(part_lo + q * 4, 0.f);
-        const int cp = tid & 15, u = tid >> 4;  // build role: column pair, low entry bits
+        for (int q = tid; q < T * 16; q += W * 32) sts_f32(part_lo + q * 4, 0.f);
+        const int cp = tid & 15, u = (tid >> 4) & 15, hb = tid >> 8;  // build role: column pair, entry bits
         const uint32_t cs = ASYM ? csum_lo : 0u;
         // build slice sl's table into segment sl & 1 from the staged x
         auto build = [&](int sl) {
@@ -304,7 +338,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
             const float4 v0 = lds_v4f(xv), v1 = lds_v4f(xv + 16), v2 = lds_v4f(xv + 32), v3 = lds_v4f(xv + 48);
             const float pa[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
             const float pb[8] = {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
-            build_cols2(pa, pb, u, cp, tbl_lo, sl & 1, cs);
+            if constexpr (W == 8) build_cols2(pa, pb, u, cp, tbl_lo, sl & 1, cs);
+            else build_cols2_half(pa, pb, u, hb, cp, tbl_lo, sl & 1, cs);
         };
 
         pdl_wait();  // x (and y) belong to the previous kernel
@@ -316,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
             const int nq = S * kChunksPerSlice;
             const XT* xg = static_cast<const XT*>(a.x);
 #pragma unroll 1
-            for (int q = tid; q < ((a.dbg & 32) ? 0 : nq); q += kW * 32) {
+            for (int q = tid; q < ((a.dbg & 32) ? 0 : nq); q += W * 32) {
                 float xq[8];
                 load_x8_any<XT>(xg, s0 * kSliceCols + q * 8, a.cols, a.glu, xq);
                 const uint32_t d = xs_lo + (uint32_t)(q * 32);
@@ -326,11 +361,11 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
                 sts_v2(d + 24, xq[6], xq[7]);
             }
         }
-        bar_consumers();
+        bar_consumers<W>();
         if (tid == 0) ABCQ_CTRACE(9);
 #pragma unroll 1
         for (int sl = 0; sl < S && sl < 2 && !(a.dbg & 4); ++sl) build(sl);
-        bar_consumers();
+        bar_consumers<W>();
         if (tid == 0) ABCQ_CTRACE(2);
 
         int slot = 0;
@@ -371,9 +406,9 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
 #pragma unroll 1
             for (int k = 0; k < nch; ++k) {
                 const int ta = k * T / nch, tb = (k + 1) * T / nch;
-                const int nt = tb - ta;  // chunk tiles; this warp takes q = warp (and warp + kW)
-                const bool v0 = warp < nt, v1 = warp + kW < nt;
-                const uint32_t q0 = (uint32_t)(v0 ? warp : 0), q1 = (uint32_t)(v1 ? warp + kW : 0);
+                const int nt = tb - ta;  // chunk tiles; this warp takes q = warp (and warp + W)
+                const bool v0 = warp < nt, v1 = warp + W < nt;
+                const uint32_t q0 = (uint32_t)(v0 ? warp : 0), q1 = (uint32_t)(v1 ? warp + W : 0);
                 float acc0 = 0.f, acc1 = 0.f;
                 mbar_wait(&full[slot], ph);
                 const uint32_t st = ring_lo + (uint32_t)(slot * a.stage_bytes);
@@ -408,22 +443,22 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
                         sts_f32(pa, lds_f32_at(pa) + r0v);
                     }
                     if (v1) {
-                        const uint32_t pa = part_lo + ((ta + warp + kW) * 16 + lane) * 4;
+                        const uint32_t pa = part_lo + ((ta + warp + W) * 16 + lane) * 4;
                         sts_f32(pa, lds_f32_at(pa) + r1v);
                     }
                 }
             }
             if (sl + 1 < S && S > 2) {
-                bar_consumers();  // all warps done with segment sl&1; publishes the build of slice sl+1
+                bar_consumers<W>();  // all warps done with segment sl&1; publishes the build of slice sl+1
                 if (sl + 2 < S) build(sl + 2);
             }
         }
-        bar_consumers();  // all row partials of this CTA written
+        bar_consumers<W>();  // all row partials of this CTA written
         if (tid == 0) ABCQ_CTRACE(3);
         if (C == 1) {
             YT* y = static_cast<YT*>(a.y);
             const int r0 = t0 * kTileRows, r1 = min(t1 * kTileRows, a.rows);
-            for (int row = r0 + tid; row < r1; row += kW * 32) y[row] = from_f32<YT>(lds_f32_at(part_lo + (row - r0) * 4));
+            for (int row = r0 + tid; row < r1; row += W * 32) y[row] = from_f32<YT>(lds_f32_at(part_lo + (row - r0) * 4));
         }
     }
     if (C > 1 && !(a.dbg & 8)) {
@@ -434,8 +469,8 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         const int r0 = t0 * kTileRows, nr = min(t1 * kTileRows, a.rows) - r0;
         const int rpr = (nr + C - 1) / C;  // rows per rank
         const uint32_t recv_lo = lo_base + a.recv_off;
-        if (warp < kW) {
-            for (int q = tid; q < nr; q += kW * 32) {
+        if (warp < W) {
+            for (int q = tid; q < nr; q += W * 32) {
                 const int c = q / rpr;
                 uint32_t ra;
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
@@ -446,10 +481,10 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_cluster_kernel(const __grid_
         }
         cluster_sync_all();  // every rank's pushes landed
         if (tid == 0) ABCQ_CTRACE(10);
-        if (warp < kW) {
+        if (warp < W) {
             YT* y = static_cast<YT*>(a.y);
             const int lo = rank * rpr, hi_r = min(nr, lo + rpr);
-            for (int q = lo + tid; q < hi_r; q += kW * 32) {
+            for (int q = lo + tid; q < hi_r; q += W * 32) {
                 float sum = lds_f32_at(recv_lo + (uint32_t)((q - lo) * 4));
                 for (int c = 1; c < C; ++c) sum += lds_f32_at(recv_lo + (uint32_t)((c * rpr + q - lo) * 4));
                 y[r0 + q] = from_f32<YT>(sum);

@@ -48,6 +48,7 @@ int launch_gemv_cluster(const abcq_model_t* m, int p, const void* x, int x_dtype
                         cudaStream_t st);
 int gemv_cluster_geometry(const abcq_model_t* m, int p, int* out7);
 extern int g_cl_force;
+extern int g_cl_warps;
 
 // small-batch mixed-precision GEMM (tensor cores), B <= 16
 size_t gemm_workspace_bytes(const abcq_model_t* m, int B);

@@ -370,7 +370,8 @@ def test_cluster_gemv_geometries_vs_oracle(P, rows, cols, asym, sd):
         want[p] = O.gemv_lut(m.bitplanes.words, cols, 128, a, z, p, xf)
     try:
         L.abcq_debug_set_mode(27)  # every shape through the cluster kernel
-        for force in CLUSTER_FORCE:
+        for force, warps in [(f, 6000) for f in CLUSTER_FORCE] + [(5162, 6008), (5142, 6008), (5112, 6008)]:
+            L.abcq_debug_set_mode(warps)     # consumer warps: automatic, or 8 with one CTA per SM
             L.abcq_debug_set_mode(force)
             for p in (1, 2, 4, 5):
                 y = dm.gemv(p, xd)
@@ -379,6 +380,7 @@ def test_cluster_gemv_geometries_vs_oracle(P, rows, cols, asym, sd):
                 assert torch.equal(y, dm.gemv(p, xd)), (force, p)   # bitwise repeatable
     finally:
         L.abcq_debug_set_mode(5000)
+        L.abcq_debug_set_mode(6000)
         L.abcq_debug_set_mode(0)
 
 

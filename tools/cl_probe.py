@@ -134,7 +134,10 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
         L.abcq_debug_set_mode(23)
         t_old = time_graph(models, p, x, y, a.iters)
         L.abcq_debug_set_mode(0)
-        r = {"geom": geom(base, p), "rel_vs_batch_kernel": rel(y_new, y_old),
+        L.abcq_debug_set_mode(6008)
+        t_w8 = time_graph(models, p, x, y, a.iters)
+        L.abcq_debug_set_mode(6000)
+        r = {"geom": geom(base, p), "rel_vs_batch_kernel": rel(y_new, y_old), "us_w8": round(t_w8, 3),
              "deterministic": bool(torch.equal(y_new, y_new2)),
              "us": round(t_new, 3), "GBps": round(byts / t_new / 1e3, 1),
              "frac": round(byts / t_new / 1e3 / 6553.3, 4),
@@ -143,7 +146,7 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
             sw = {}
             L.abcq_debug_set_mode(27)
             for slots in (1, 2):
-                for Cc in (8, 6):
+                for Cc in (2, 4, 8, 6):
                     for tcw in (2,):
                         L.abcq_debug_set_mode(5000 + 100 * slots + 10 * Cc + tcw)
                         gm = geom(base, p)

@@ -450,10 +450,10 @@ def run_gpu(args):
             except Exception:
                 traffic = None
         cpu = cpu_baseline() if world == 1 and not args.no_cpu else None
-        config = bench_config(world)
-        config["timing"] = ("the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream"
-                            if not mp else "eager steps, one NCCL all-gather of the step's 21 outputs per step "
-                            "overlapping the next step (double-buffered), CUDA events, max over ranks")
+        config = bench_config(world)  # (identical to the reference arm's: same_config)
+        timing = ("the K steps captured as CUDA graphs of <= 50 steps, CUDA events on the launch stream"
+                  if not mp else "eager steps, one NCCL all-gather of the step's 21 outputs per step "
+                  "overlapping the next step (double-buffered), CUDA events, max over ranks")
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -461,6 +461,7 @@ def run_gpu(args):
             "dtype_note": DTYPE_NOTE,
             "data": "synthetic (splitmix64 planes, |N(0,1)| fp16 scales, N(0,1) fp16 x)",
             "config": config,
+            "timing": timing,
             # per step: the persistent batched GEMV kernel + the split-K reduce kernel
             "gpu_launches": args.steps * 2,
             "parity": parity,

@@ -136,10 +136,13 @@ class _Attention:
         return self.out
 
 
+PERSISTENT_QKV_O = True  # (tools/decode_ab.py --cluster-qkv-o measures the alternative)
+
+
 def _persistent(m, p, x, out):
     """One GEMV through the persistent batch kernel (a batch of one); other
     linear objects (e.g. a dense test reference) through their own gemv()."""
-    if isinstance(m, DeviceModel):
+    if isinstance(m, DeviceModel) and PERSISTENT_QKV_O:
         gemv_batch([(m, p, x, out)])
     else:
         m.gemv(p, x, out=out)

@@ -106,3 +106,29 @@ def test_service_gemv_per_request_precision(tmp_path):
     assert client.post("/models/m/gemv", json={"precision": 2, "x": [0.0] * 7}).status_code == 400
     r = client.post("/models/m/bench", json={"precisions": [2], "repeats": 2})
     assert r.status_code == 200 and r.json()["rows"] == 128
+
+
+def test_graph_capture_during_progressive_upload_raises():
+    """A CUDA graph captured while a precision's planes are still uploading would
+    replay reads of bytes that have not landed: it is refused."""
+    import torch
+
+    import paper_2510_10467_b200 as P
+    dm = P.DeviceModel(64, 256, 128, 2, 2, scale_dtype="f16")
+    dm.load_planes(torch.randint(-2**31, 2**31 - 1, (2, 64, 8), dtype=torch.int32, device="cuda"))
+    dm.load_scale_set(2, torch.rand((2, 64, 2), device="cuda") * 0.1)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(200_000_000)       # an upload still in flight on the side stream
+        ev = torch.cuda.Event()
+        ev.record(side)
+    dm.mark_level_ready(2, ev)
+    x = torch.randn(256, device="cuda").half()
+    st = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(P.UsageError):
+        with torch.cuda.graph(g, stream=st):
+            dm.gemv(2, x)
+    torch.cuda.synchronize()
+    y = dm.gemv(2, x)                        # resident now: serves
+    assert torch.isfinite(y).all()

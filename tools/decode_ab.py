@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--modes", default="0,23")
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--cluster-qkv-o", action="store_true", help="also time q/k/v and o through abcq_gemv (cluster kernel)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 qm = QuantizedLlamaStep(LlamaConfig(layers=a.layers), p=3, ctx=1024)
@@ -31,3 +32,12 @@ for spec in a.modes.split(","):
         out[f"mode{mode}_p{p}_ms"] = round(time_step(qm, a.iters), 4)
     print(json.dumps(out), flush=True)
 _lib.lib().abcq_debug_set_mode(0)
+if a.cluster_qkv_o:
+    import paper_2510_10467_b200.decode as D
+    for flag in (False, True, False, True):
+        D.PERSISTENT_QKV_O = flag
+        for p in (2, 3, 4):
+            qm.p = p
+            out[f"{'persistent' if flag else 'cluster'}_qkv_o_p{p}_ms"] = round(time_step(qm, a.iters), 4)
+        print(json.dumps(out), flush=True)
+    D.PERSISTENT_QKV_O = True

@@ -206,14 +206,15 @@ class DeviceModel:
         ev = self._level_ready.get(p)
         if ev is None:
             return
+        if torch.cuda.is_current_stream_capturing():
+            # a graph captured now could replay reads of planes / scales that
+            # have not landed (the kernels prefetch weights before their PDL
+            # wait), and the upload event cannot be queried under capture
+            raise UsageError(f"precision {p} was uploaded progressively and not yet confirmed resident; "
+                             "run one call (or synchronize) before capturing CUDA graphs")
         if ev.query():  # upload finished: no ordering needed from now on
             del self._level_ready[p]
             return
-        if torch.cuda.is_current_stream_capturing():
-            # a graph captured now would replay reads of planes / scales that
-            # have not landed (the kernels prefetch weights before their PDL wait)
-            raise UsageError(f"precision {p} is still uploading; capture CUDA graphs once the model is "
-                             "resident (synchronize the upload first)")
         (stream if stream is not None else torch.cuda.current_stream(self.device)).wait_event(ev)
 
     def struct_ptr(self):

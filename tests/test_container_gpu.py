@@ -130,5 +130,8 @@ def test_graph_capture_during_progressive_upload_raises():
         with torch.cuda.graph(g, stream=st):
             dm.gemv(2, x)
     torch.cuda.synchronize()
-    y = dm.gemv(2, x)                        # resident now: serves
+    y = dm.gemv(2, x)                        # resident now: serves (and confirms the level)
     assert torch.isfinite(y).all()
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2, stream=st):    # ... after which capture works
+        dm.gemv(2, x)

@@ -166,9 +166,11 @@ bool cluster_supports(const abcq_model_t* m, int p) {
     // cluster kernel wins while a GEMV is latency-bound -- up to ~24 MB of plane
     // bytes and <= 2 slices per CTA at C = 16; larger GEMVs stream better
     // through the persistent batch kernel (more CTAs, deeper rings)
-    if (g_dbg_mode != 27) {  // (27: every single GEMV through the cluster kernel -- test coverage)
+    // (27: every single GEMV through the cluster kernel -- test coverage;
+    //  28: any size up to 32 slices -- experiments)
+    if (g_dbg_mode != 27) {
         const int64_t plane_bytes = (int64_t)p * tiled_plane_bytes(m->rows, m->cols);
-        if (n_slices(m->cols) > 32 || plane_bytes > (int64_t)24 * 1024 * 1024) return false;
+        if (n_slices(m->cols) > 32 || (g_dbg_mode != 28 && plane_bytes > (int64_t)24 * 1024 * 1024)) return false;
     }
     cl::Geom g;
     return cl::plan(m, p, g);

@@ -145,9 +145,10 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
         if a.sweep:
             sw = {}
             L.abcq_debug_set_mode(27)
-            for slots in (1, 2):
-                for Cc in (2, 4, 8, 6):
-                    for tcw in (2,):
+            for slots, warps in ((1, 6016), (1, 6008)):
+                L.abcq_debug_set_mode(warps)
+                for Cc in (4, 8, 6):
+                    for tcw in (1, 2):
                         L.abcq_debug_set_mode(5000 + 100 * slots + 10 * Cc + tcw)
                         gm = geom(base, p)
                         if gm is None:
@@ -157,10 +158,11 @@ for (rows, cols) in ([] if (__import__('os').environ.get('CL_TIMELINE') or __imp
                             torch.cuda.synchronize()
                             ok = rel(yy, y_old)
                             t = time_graph(models, p, x, y, a.iters)
-                            sw[f"s{slots}C{Cc}t{tcw}"] = [round(t, 3), f"{ok:.1e}", gm]
+                            sw[f"s{slots}C{Cc}t{tcw}w{warps - 6000}"] = [round(t, 3), f"{ok:.1e}", gm]
                         except Exception as e:  # noqa: BLE001
-                            sw[f"s{slots}C{Cc}t{tcw}"] = str(e)[:80]
+                            sw[f"s{slots}C{Cc}t{tcw}w{warps - 6000}"] = str(e)[:80]
             L.abcq_debug_set_mode(5000)
+            L.abcq_debug_set_mode(6000)
             L.abcq_debug_set_mode(0)
             r["sweep"] = sw
         rec[f"p{p}"] = r

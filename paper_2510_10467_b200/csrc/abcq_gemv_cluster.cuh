@@ -284,12 +284,14 @@ __global__ void __launch_bounds__(threads_of<W>(), (W == 8 ? 2 : 1)) gemv_cluste
     if (warp == W) {
         // ---------------- producer: weights/scales never depend on the previous kernel
         if (lane == 0 && nst > 0) {
+            ABCQ_CTRACE(11);
             const uint64_t pol = l2_evict_first_policy();
             const int esz = (int)sizeof(ST);
             int sl = 0, k = 0, slot = 0;
             uint32_t ph = 0;
             const uint32_t wsz = (uint32_t)(a.tc * kBlockBytes), ssz = (uint32_t)(a.tc * 32 * esz);
             for (int e = 0; e < nst; ++e) {
+                if (e == 1) ABCQ_CTRACE(12);
                 if (e >= R) mbar_wait(&empty[slot], ph ^ 1u);
                 const int s = s0 + sl;
                 const int ta = t0 + k * T / nch, tb = t0 + (k + 1) * T / nch;
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(threads_of<W>(), (W == 8 ? 2 : 1)) gemv_cluste
                 const uint32_t q0 = (uint32_t)(v0 ? warp : 0), q1 = (uint32_t)(v1 ? warp + W : 0);
                 float acc0 = 0.f, acc1 = 0.f;
                 mbar_wait(&full[slot], ph);
+                if (tid == 0 && sl == 0 && k == 0) ABCQ_CTRACE(13);
                 const uint32_t st = ring_lo + (uint32_t)(slot * a.stage_bytes);
                 if ((a.dbg & 1) == 0 && v0) {
                     // two tiles x two planes per group (one code path: a warp

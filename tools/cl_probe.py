@@ -233,7 +233,8 @@ def timeline(rows, cols, p, mode=5000, dbg=0, n=8):
         f = lambda k, fn: round((int(fn(ts[:, k])) - t0) / 1e3, 2)  # noqa: E731
         rows_out.append({"start": [f(0, min), f(0, max)], "prod_done": f(8, max), "wait": [f(1, min), f(1, max)],
                          "x_staged": f(9, max), "tables": f(2, max), "first_stage": [f(5, min), f(5, max)],
-                         "last_stage": f(7, max), "stream": f(3, max), "cl_bar": f(10, max),
+                         "prod_begin": f(11, max), "prod_first_issued": f(12, max), "first_full": f(13, max),
+                         "stream": f(3, max), "cl_bar": f(10, max),
                          "end": [f(4, min), f(4, max)],
                          "smids": len(set(int(v) for v in ts[:, 6]))})
     L.abcq_debug_set_mode(5000)

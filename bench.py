@@ -935,33 +935,45 @@ def config5_row_sharded(ctx, args, peak):
                     e.local(p, e.x_buffer, ctx.stream)
 
         gemv_ms = ctx.time_graph(local_all, reps=10)
-        # + the all-gather of every layer's output (eager; the max over ranks)
-        with torch.cuda.stream(ctx.stream):
-            for _ in range(3):
-                for e in engines:
+
+        def local_gather_all():
+            for e in engines:
+                if e is not None:
                     e.local(p, e.x_buffer, ctx.stream)
                     e.gather()
-        torch.cuda.synchronize()
+
+        # + the all-gather of every layer's output: captured in the graph too
+        # (NCCL over NVLink); eager with events if capture is refused
         if world > 1:
             dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 10
-        with torch.cuda.stream(ctx.stream):
-            a.record(ctx.stream)
-            for _ in range(n):
-                for e in engines:
-                    e.local(p, e.x_buffer, ctx.stream)
-                    e.gather()
-            b.record(ctx.stream)
-        torch.cuda.synchronize()
-        full_ms = a.elapsed_time(b) / n
+        try:
+            full_ms = ctx.time_graph(local_gather_all, reps=10)
+            mode = "graph"
+        except Exception:  # noqa: BLE001
+            torch.cuda.synchronize()
+            with torch.cuda.stream(ctx.stream):
+                for _ in range(3):
+                    local_gather_all()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = 10
+            with torch.cuda.stream(ctx.stream):
+                a.record(ctx.stream)
+                for _ in range(n):
+                    local_gather_all()
+                b.record(ctx.stream)
+            torch.cuda.synchronize()
+            full_ms = a.elapsed_time(b) / n
+            mode = "eager"
         t = torch.tensor([gemv_ms, full_ms], device=ctx.dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         gemv_ms, full_ms = (float(v) for v in t.tolist())
         total = sum(algo_bytes(r, k, p) for _, r, k in LAYERS_70B)
         res[f"p{p}"] = {"gemv_us_per_layer_set": round(gemv_ms * 1e3, 2),
-                        "gemv_allgather_us_per_layer_set": round(full_ms * 1e3, 2),
+                        "gemv_allgather_us_per_layer_set": round(full_ms * 1e3, 2), "allgather_timing": mode,
                         "GBps_total": round(total / (gemv_ms * 1e-3) / 1e9, 1),
                         "roofline_frac_per_gpu": round(total / world / (gemv_ms * 1e-3) / 1e9 / peak, 4)}
     del engines

@@ -56,8 +56,9 @@ class RowShardedGemv:
     Every rank passes the same full model (or only its shard, `shard=` with
     `rows=` the full row count), calls `gemv(p, x)` with the same x, and
     receives the full y. All buffers are allocated once: the rank's slice is
-    written by a GemvBatchPlan launch (one C-ABI call) straight into the
-    all-gather send buffer, and y is a view of the gather's receive buffer --
+    written by one abcq_gemv launch (the cluster kernel for a small shard, the
+    persistent kernel for a large one) straight into the all-gather send
+    buffer, and y is a view of the gather's receive buffer --
     shards sit on 16-row tile boundaries with every rank but the last holding
     exactly `pad_rows` rows, so the gathered buffer's first `rows` elements
     ARE y in order (no per-call allocation, copy or concatenation).
@@ -100,16 +101,7 @@ class RowShardedGemv:
         self._local = local_gemv
         self._send = torch.zeros(self.pad_rows, dtype=dtype, device=self.device)
         self._recv = torch.empty(self.pad_rows * self.world, dtype=dtype, device=self.device)
-        self._x = torch.empty(self.cols, dtype=dtype, device=self.device)  # the plans' fixed input
-        self._plans = {}
-
-    def _plan(self, p: int):
-        plan = self._plans.get(p)
-        if plan is None:
-            from .device_model import GemvBatchPlan
-
-            plan = self._plans[p] = GemvBatchPlan([(self.dm, p, self._x, self._send[: self.shard_rows])])
-        return plan
+        self._x = torch.empty(self.cols, dtype=dtype, device=self.device)  # the fixed input buffer
 
     def local(self, p: int, x: torch.Tensor, stream=None) -> None:
         """This rank's slice of y into the send buffer (no communication)."""
@@ -124,7 +116,7 @@ class RowShardedGemv:
             return
         if x.data_ptr() != self._x.data_ptr():
             self._x.copy_(x.reshape(-1))
-        self._plan(p).launch(stream)
+        self.dm.gemv(p, self._x, out=self._send[: self.shard_rows], stream=stream)
 
     def gather(self, async_op: bool = False):
         """All-gather the slices; y = self.y (a view of the receive buffer)."""

@@ -18,7 +18,6 @@ only the results (packed words, f32 scales) come back to the host.
 
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -27,8 +26,7 @@ import torch
 from . import _lib
 from .device_model import _stream_handle, require_cuda
 from .errors import NonFiniteError, UsageError
-from .model import (BitPlaneSet, MultiPrecisionModel, QuantConfig, ScaleTensor, group_count, pack_signs,
-                    words_per_row)
+from .model import BitPlaneSet, MultiPrecisionModel, QuantConfig, ScaleTensor, group_count, words_per_row
 
 MAX_PLANES = _lib.ABCQ_MAX_PLANES
 MAX_GROUP = 1024
@@ -124,19 +122,23 @@ class _Fit:
         return plane
 
     def dequant(self, codes, alpha, offset):
-        """_dequant64 (bcq.py:137-152) on the device: planes ascending, offset last."""
-        q = codes.shape[0]
-        idx = torch.arange(self.cols, device=self.dev) // self.g
-        rec = torch.zeros((self.rows, self.cols), dtype=torch.float64, device=self.dev)
-        for i in range(q):
-            rec += codes[i].to(torch.float64) * alpha[i][:, idx]
-        if offset is not None:
-            rec += offset[:, idx]
-        return rec
+        return _dequant64(codes, alpha, offset, self.g)
 
     def sq_error(self, codes, alpha, offset) -> float:
         d = self.w - self.dequant(codes, alpha, offset)
         return float((d * d).sum())
+
+
+def _dequant64(codes, alpha, offset, g: int) -> torch.Tensor:
+    """_dequant64 (bcq.py:137-152) on the device: planes ascending, offset last."""
+    q, rows, cols = codes.shape
+    idx = torch.arange(cols, device=codes.device) // g
+    rec = torch.zeros((rows, cols), dtype=torch.float64, device=codes.device)
+    for i in range(q):
+        rec += codes[i].to(torch.float64) * alpha[i][:, idx]
+    if offset is not None:
+        rec += offset[:, idx]
+    return rec
 
 
 def _pack(codes: torch.Tensor) -> BitPlaneSet:
@@ -238,9 +240,7 @@ def dequantize(qm: QuantizedMatrix, p: int) -> np.ndarray:
     alpha = torch.from_numpy(qm.scales.alpha[:p].astype(np.float64)).to(dev)
     off = qm.scales.offset
     offset = None if off is None else torch.from_numpy(off.astype(np.float64)).to(dev)
-    f = _Fit.__new__(_Fit)
-    f.dev, (f.rows, f.cols), f.g = dev, qm.shape, qm.config.group_size
-    return f.dequant(codes, alpha, offset).to(torch.float32).cpu().numpy()
+    return _dequant64(codes, alpha, offset, qm.config.group_size).to(torch.float32).cpu().numpy()
 
 
 def relative_reconstruction_error(w, qm: QuantizedMatrix, p: int | None = None) -> float:

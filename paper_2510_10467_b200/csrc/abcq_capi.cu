@@ -77,6 +77,10 @@ extern "C" {
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
 int abcq_debug_set_mode(int32_t mode) {
+    if (mode >= 7000 && mode < 7000 + 1 + 255) {  // batch kernel round trace of CTA mode - 7001 (7000 = off)
+        abcq::g_rtrace_cta = mode - 7001;
+        return 0;
+    }
     if (mode >= 6000 && mode < 6100) {  // cluster GEMV consumer warps: 6000 + W (8 / 16; 6000 = automatic)
         abcq::g_cl_warps = mode - 6000;
         return 0;

@@ -65,6 +65,8 @@ struct KArgs {
     int prefill;  // ring slots issued before the PDL wait
     int dbg;      // profiling experiments: 1 = skip the lookups
     unsigned long long* trace;
+    unsigned long long* rtrace;  // per-warp round stamps of CTA rtrace_cta (profiling), or NULL
+    int rtrace_cta;
 };
 
 struct BatchArgs {
@@ -79,6 +81,8 @@ struct BatchArgs {
     int prefill;
     int dbg;
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
+    unsigned long long* rtrace;
+    int rtrace_cta;
 };
 
 template <typename ST, bool ASYM>
@@ -161,6 +165,39 @@ __device__ __forceinline__ WarpRun warp_run(const KArgs<NJ>& a, const Round& R, 
     return w;
 }
 static_assert(kWarps == 16, "warp_run divides by kWarps with a shift");
+// Chunk-aligned split of a one-piece round (default; debug mode 32 = the cost
+// split above): the piece's ceil(n / KK) slot-sized chunks go to the warps in
+// rank order -- rank = (warp - off) mod 16, off = the CTA's chunk count before
+// this piece, so successive short pieces land on successive warps -- one
+// chunk per rank while there are fewer chunks than warps, else contiguous
+// runs of floor / ceil(chunks / 16). Every slot but a piece's last is full:
+// in the saturated memory system a warp's share of HBM bandwidth follows its
+// bytes in flight, and the cost split left warps of short pieces (k / v
+// slices of a few row tiles per CTA) with half-filled slots streaming at
+// half rate (per-round stamps, tools/layer_probe.py --rtrace). Warps without
+// a chunk run on into the next round (its table is already built). A CTA of
+// ONE round keeps the cost split: no round follows for idle warps, and there
+// more warps with part-filled slots keep more bytes in flight (single-GEMV
+// CTAs of one short piece: decode p3 2.21 -> 2.28 ms/token with chunks).
+template <int KK>
+__device__ __forceinline__ WarpRun warp_run_chunks(const Round& R, int warp, int it0) {
+    const int lo = R.pc[0].lo, n = R.pc[0].hi - lo;
+    const int c = (n + KK - 1) / KK;
+    const int off = ((lo - it0) / KK) & 15;
+    const int w = (warp - off) & 15;
+    int c0, c1;
+    if (c <= 16) {
+        c0 = min(w, c);
+        c1 = min(w + 1, c);
+    } else {
+        c0 = (w * c) >> 4;
+        c1 = ((w + 1) * c) >> 4;
+    }
+    WarpRun r;
+    r.lo = lo + min(c0 * KK, n);
+    r.hi = lo + min(c1 * KK, n);
+    return r;
+}
 __device__ __forceinline__ int sub_lo(const WarpRun& w, const Round& R, int k) {
     return k == 0 ? w.lo : max(w.lo, R.pc[0].hi);
 }
@@ -381,7 +418,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     auto enter_round = [&](Cur& k, int rs) {
         for (; rs < it1;) {
             const Round Rn = make_round(a, rs, it1);
-            const WarpRun wr = warp_run(a, Rn, warp);
+            const WarpRun wr = (a.dbg == 32 || (Rn.pc[0].lo == it0 && Rn.end >= it1)) ? warp_run(a, Rn, warp) : warp_run_chunks<kK>(Rn, warp, it0);
             k.rs = rs;
             k.rend = Rn.end;
             k.mid = Rn.pc[0].hi;
@@ -570,13 +607,20 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
         __syncthreads();
     }
     if (warp == 0) ABCQ_BTRACE(2);
+#define ABCQ_RTRACE(k)                                                                          \
+    do {                                                                                        \
+        if (a.rtrace && (int)blockIdx.x == a.rtrace_cta && lane == 0 && round < 32)             \
+            a.rtrace[(warp * 32 + round) * 4 + (k)] = globaltimer();                            \
+    } while (0)
     for (int rs = it0; rs < it1; ++round) {
         const Round Rd = make_round(a, rs, it1);
+        ABCQ_RTRACE(0);
         if (round >= 2) {  // table of round `round` (built by the last warp of round-2)
             while (ready[round & 1] < round) __nanosleep(64);
             __threadfence_block();
         }
-        const WarpRun wr = warp_run(a, Rd, warp);
+        ABCQ_RTRACE(1);
+        const WarpRun wr = (a.dbg == 32 || (Rd.pc[0].lo == it0 && Rd.end >= it1)) ? warp_run(a, Rd, warp) : warp_run_chunks<kK>(Rd, warp, it0);
         // builder of round+2's table? then fetch its x now (used after this round)
         const bool builder = (warp >> 2) == (round & 3);
         bool build_next = false;
@@ -686,10 +730,12 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             run(std::integral_constant<int, 0>{});
         // done with round `round`; builders fill round+2's table into this half
         __syncwarp();
+        ABCQ_RTRACE(2);
         if (lane == 0) atomicAdd((int*)&done[round & 1], 1);
         if (build_next) {
             while (done[round & 1] < kWarps) __nanosleep(32);
             __threadfence_block();
+            ABCQ_RTRACE(3);
 #pragma unroll
             for (int k = 0; k < 4; ++k) build_entries(bx, round & 1, lane, (warp & 3) * 4 + k);
             __syncwarp();
@@ -763,6 +809,8 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     a.prefill = ba.prefill;
     a.dbg = ba.dbg;
     a.trace = ba.trace;
+    a.rtrace = ba.rtrace;
+    a.rtrace_cta = ba.rtrace_cta;
     int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/4) per job)
     constexpr int kFusedRows = kBThreads / kReduceTPR;
     for (int j = 0; j < ba.n_jobs; ++j)

@@ -11,6 +11,7 @@
 namespace abcq {
 
 unsigned long long* g_trace = nullptr;  // abcq_debug_set_trace (profiling aid)
+int g_rtrace_cta = -1;
 int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experiments)
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
@@ -207,9 +208,12 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             }
     }
     a.prefill = g_prefill;
-    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22) ? g_dbg_mode : 0;
+    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22 || g_dbg_mode == 32) ? g_dbg_mode : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
+    // round trace: after the 16 launch slots, [warp][round < 32][4] stamps of CTA g_rtrace_cta
+    a.rtrace = g_trace && g_rtrace_cta >= 0 ? g_trace + (size_t)16 * kTraceCtas * 8 : nullptr;
+    a.rtrace_cta = g_rtrace_cta;
     const abcq_model_t* m = models[0];
     const bool asym = m->asymmetric != 0;
     return x_dtypes[0] != ABCQ_F32 ? launch_yt<__half>(a, y_dtype, m->scale_dtype, asym, grid, st)

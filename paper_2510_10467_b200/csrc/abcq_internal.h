@@ -87,6 +87,7 @@ int launch_fit_residual_sign(const double* w, const int8_t* codes, const double*
                              int rows, int cols, int g, int8_t* plane, cudaStream_t st);
 
 extern unsigned long long* g_trace;
+extern int g_rtrace_cta;  // abcq_debug_set_mode(7001 + cta): per-warp round stamps of one batch-kernel CTA
 extern int g_dbg_mode;
 extern int g_piece_blocks;
 extern int g_prefill;

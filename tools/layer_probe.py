@@ -29,6 +29,8 @@ ap.add_argument("--copies", type=int, default=3)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--piece", type=int, default=-1, help="piece cost in blocks (load-balance model)")
 ap.add_argument("--mixed", action="store_true", help="jobs at p=2,3,4 in one launch (bench step)")
+ap.add_argument("--pad", type=int, default=0, help="extra bytes between planes (plane stride experiment)")
+ap.add_argument("--rtrace", default="", help="comma list of CTAs: per-warp round stamps (debug mode 7001 + cta)")
 a = ap.parse_args()
 signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under | head
 torch.cuda.set_device(0)
@@ -40,6 +42,10 @@ for c in range(a.copies):
     for li in sel:
         _, r, k = LAYERS[li]
         dm = P.DeviceModel(r, k, 128, 2, 4, False, scale_dtype="f16")
+        if a.pad:
+            dm.plane_stride += a.pad
+            dm.planes = torch.zeros(dm.p_hi * dm.plane_stride, dtype=torch.uint8, device="cuda")
+            dm._refresh_struct()
         dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, r, k // 32), dtype=torch.int32, device="cuda",
                                      generator=g))
         for p in (2, 3, 4):
@@ -85,7 +91,7 @@ print(f"jobs {[LAYERS[li][0] for li in sel]} p={PS}: {us:.2f} us/launch, {byts /
       f"{byts / us / 1e3:.0f} GB/s")
 
 SL = 168 * 8
-buf = torch.zeros(16 * SL, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * SL + 16 * 32 * 4, dtype=torch.int64, device="cuda")
 _lib.lib().abcq_debug_set_trace(buf.data_ptr())
 g3 = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g3, stream=st):
@@ -96,10 +102,10 @@ with torch.cuda.stream(st):
     g3.replay()
     torch.cuda.synchronize()
     buf.zero_()
-    buf.view(16, 168, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
+    buf[:16 * SL].view(16, 168, 8)[:, 148, 0:2] = 1 << 62  # reduce kernel: atomicMin slots
     g3.replay()
 torch.cuda.synchronize()
-t = buf.view(16, 168, 8).cpu().numpy()
+t = buf[:16 * SL].view(16, 168, 8).cpu().numpy()
 used = [k for k in range(16) if t[k, :148, 0].max() > 0]
 used.sort(key=lambda k: t[k, :148, 0][t[k, :148, 0] > 0].min())
 t0 = t[used[0], :148, 0][t[used[0], :148, 0] > 0].min()
@@ -121,6 +127,36 @@ for k in used:
             " ".join(f"{(arr[i] - t0) / 1e3:.1f}/{(tstart[i] - t0) / 1e3:.1f}/{(wpass[i] - t0) / 1e3:.1f}/{(v - t0) / 1e3:.1f}"
                      for i, v in enumerate(jobs) if v > 0)))
     print("  " + " | ".join(row))
+# per-warp round stamps of selected CTAs (one more traced graph per CTA)
+for cta in [int(v) for v in a.rtrace.split(",") if v]:
+    _lib.lib().abcq_debug_set_mode(7001 + cta)
+    _lib.lib().abcq_debug_set_trace(buf.data_ptr())
+    g4 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g4, stream=st):
+        for i in range(4):
+            launch(i % a.copies)
+    _lib.lib().abcq_debug_set_trace(None)
+    _lib.lib().abcq_debug_set_mode(7000)
+    with torch.cuda.stream(st):
+        g4.replay()
+        torch.cuda.synchronize()
+        buf.zero_()
+        g4.replay()
+    torch.cuda.synchronize()
+    tb = buf.view(-1).cpu().numpy()
+    R4 = tb[16 * SL:].reshape(16, 32, 4).astype(np.float64)
+    T = tb[:16 * SL].reshape(16, 168, 8)
+    lastk = max(range(16), key=lambda k: T[k, cta, 0])
+    c0 = float(T[lastk, cta, 0])
+    print(f"  CTA {cta} rounds (us from CTA start; per round: start min/max | table ok max | run done min/max | build start max)")
+    for r in range(32):
+        col = R4[:, r, :]
+        if col[:, 0].max() <= 0:
+            break
+        f = lambda k, fn: (fn(col[:, k][col[:, k] > 0]) - c0) / 1e3 if (col[:, k] > 0).any() else float("nan")
+        print(f"    r{r:2d}: start {f(0, np.min):6.2f}/{f(0, np.max):6.2f} | tbl {f(1, np.max):6.2f} | "
+              f"done {f(2, np.min):6.2f}/{f(2, np.max):6.2f} | build {f(3, np.max):6.2f}")
+
 # per-CTA detail of the last launch: stream duration (tab0 -> streamed) vs rounds
 T = t[used[-1], :148].astype(np.float64)
 dur = (T[:, 3] - T[:, 2]) / 1e3
@@ -132,6 +168,21 @@ for nr in sorted(set(rounds.tolist())):
     print(f"    rounds={nr}: {m.sum():3d} CTAs, stream med {np.median(dur[m]):.2f} max {dur[m].max():.2f}")
 slow = np.argsort(-dur)[:8]
 print("  slowest CTAs:", ", ".join(f"{b}:{dur[b]:.1f}us/r{rounds[b]}" for b in slow))
+
+# does a CTA's stream time repeat across identical launches (schedule / placement) or not (noise)?
+if len(used) >= 3:
+    durs = np.array([(t[k, :148, 3].astype(np.float64) - t[k, :148, 2]) / 1e3 for k in used[1:]])
+    cc = np.corrcoef(durs)
+    print("  stream-time correlation by CTA index across launches:",
+          " ".join(f"{cc[i, j]:.2f}" for i in range(len(durs)) for j in range(i + 1, len(durs))))
+    ends = np.array([(t[k, :148, 3].astype(np.float64) - t[k, :148, 0].min()) / 1e3 for k in used[1:]])
+    ce = np.corrcoef(ends)
+    print("  stream-END correlation by CTA index across launches:",
+          " ".join(f"{ce[i, j]:.2f}" for i in range(len(ends)) for j in range(i + 1, len(ends))))
+    import json as _json
+    Path("gpurun_out").mkdir(exist_ok=True)
+    Path("gpurun_out/lp_cta_durs.json").write_text(_json.dumps({"durs": durs.round(3).tolist(), "ends": ends.round(3).tolist(),
+                                                                "rounds": t[used[-1], :148, 6].tolist()}))
 
 # systematic per-SM speed? correlate stream durations of consecutive launches by SM id
 if False and len(used) >= 3:  # (needs SM ids in slot 7)

@@ -249,15 +249,23 @@ constexpr int kReduceRows = kReduceThreads / kReduceTPR * kReduceRPT;  // rows p
 template <int NJ, typename YT, int RPB, int RPT, bool RELEASE, bool PRE_WAIT = false>
 __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     constexpr int rpb = RPB;
-    int j = 0, nbj = 0;
-    for (; j < a.n_jobs; ++j) {
-        const Job& J = a.jobs[j];
-        if (J.NS <= 1) continue;
-        nbj = (J.rows + rpb - 1) / rpb;
-        if (blk < nbj) break;
-        blk -= nbj;
+    // blocks laid out job by job, jobs of more than 16 slices first: their
+    // completion is the longest, and the blocks reach SMs in index order as
+    // the GEMV CTAs retire (debug mode 29: plain job order)
+    int j = -1, nbj = 0;
+    for (int pass = (a.dbg == 29 ? 1 : 0); pass < 2 && j < 0; ++pass) {
+        for (int jj = 0; jj < a.n_jobs; ++jj) {
+            const Job& J = a.jobs[jj];
+            if (J.NS <= 1 || (pass == 0 && J.NS <= 16) || (pass == 1 && a.dbg != 29 && J.NS > 16)) continue;
+            nbj = (J.rows + rpb - 1) / rpb;
+            if (blk < nbj) {
+                j = jj;
+                break;
+            }
+            blk -= nbj;
+        }
     }
-    if (j >= a.n_jobs) {
+    if (j < 0) {
         if (PRE_WAIT) pdl_wait();
         if (RELEASE) pdl_launch_dependents();
         return;

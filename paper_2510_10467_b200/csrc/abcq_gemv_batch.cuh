@@ -175,10 +175,13 @@ static_assert(kWarps == 16, "warp_run divides by kWarps with a shift");
 // bytes in flight, and the cost split left warps of short pieces (k / v
 // slices of a few row tiles per CTA) with half-filled slots streaming at
 // half rate (per-round stamps, tools/layer_probe.py --rtrace). Warps without
-// a chunk run on into the next round (its table is already built). A CTA of
-// ONE round keeps the cost split: no round follows for idle warps, and there
-// more warps with part-filled slots keep more bytes in flight (single-GEMV
-// CTAs of one short piece: decode p3 2.21 -> 2.28 ms/token with chunks).
+// a chunk run on into the next round (its table is already built). A CTA's
+// last round keeps the cost split when it is the CTA's only round or the
+// launch is a single GEMV: no round follows for idle warps, and more warps
+// with part-filled slots keep more bytes in flight (single-GEMV CTAs of one
+// short piece: decode p3 2.21 -> 2.28 ms/token with chunks; the two-piece
+// CTAs of a 4096 x 14336 GEMV: p3 12.8 -> 13.1 us). In a batch the last
+// round is chunked too (bench step 60.6 -> 60.0 us).
 template <int KK>
 __device__ __forceinline__ WarpRun warp_run_chunks(const Round& R, int warp, int it0) {
     const int lo = R.pc[0].lo, n = R.pc[0].hi - lo;
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     auto enter_round = [&](Cur& k, int rs) {
         for (; rs < it1;) {
             const Round Rn = make_round(a, rs, it1);
-            const WarpRun wr = (a.dbg == 32 || (Rn.pc[0].lo == it0 && Rn.end >= it1)) ? warp_run(a, Rn, warp) : warp_run_chunks<kK>(Rn, warp, it0);
+            const WarpRun wr = (a.dbg == 32 || (Rn.end >= it1 && (a.n_jobs == 1 || Rn.pc[0].lo == it0))) ? warp_run(a, Rn, warp) : warp_run_chunks<kK>(Rn, warp, it0);
             k.rs = rs;
             k.rend = Rn.end;
             k.mid = Rn.pc[0].hi;
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             __threadfence_block();
         }
         ABCQ_RTRACE(1);
-        const WarpRun wr = (a.dbg == 32 || (Rd.pc[0].lo == it0 && Rd.end >= it1)) ? warp_run(a, Rd, warp) : warp_run_chunks<kK>(Rd, warp, it0);
+        const WarpRun wr = (a.dbg == 32 || (Rd.end >= it1 && (a.n_jobs == 1 || Rd.pc[0].lo == it0))) ? warp_run(a, Rd, warp) : warp_run_chunks<kK>(Rd, warp, it0);
         // builder of round+2's table? then fetch its x now (used after this round)
         const bool builder = (warp >> 2) == (round & 3);
         bool build_next = false;

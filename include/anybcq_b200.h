@@ -96,7 +96,8 @@ int abcq_debug_set_trace(void* d_buf);
  * skip the table lookups, 2 = skip the weight loads; 23 = route single GEMVs
  * through the batch kernel instead of the cluster kernel; 32 = the batch
  * kernel's round-1 warp split (cost split of every round instead of slot-sized
- * chunks); 7001 + c = per-warp round stamps of batch CTA c after the 16
+ * chunks); 33 = batch CTAs take the schedule in reverse (placement
+ * experiment); 7001 + c = per-warp round stamps of batch CTA c after the 16
  * launch slots of the trace buffer (7000 = off); 27 = route every
  * single GEMV through the cluster kernel; 5000 + 100*slots + 10*C + t = force
  * the cluster kernel's geometry (C digit 6 = 16; 5000 = automatic); 6000 + W =

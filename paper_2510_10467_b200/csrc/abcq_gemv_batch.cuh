@@ -128,10 +128,16 @@ struct WarpRun {
     int lo, hi;  // batch items; sub-run k = [lo, hi) intersected with piece k
 };
 
+// the schedule slot of this CTA: its index, or reversed under debug mode 33
+// (placement experiment: does a slow range follow the work or the SM?)
+template <int NJ>
+__device__ __forceinline__ int cta_slot(const KArgs<NJ>& a) {
+    return a.dbg == 33 ? a.main_ctas - 1 - (int)blockIdx.x : (int)blockIdx.x;
+}
 template <int NJ>
 __device__ __forceinline__ Piece piece_at(const KArgs<NJ>& a, int g, int it1) {
     Piece P;
-    P.j = a.cta_j0[blockIdx.x];  // g >= this CTA's first item: no scan from job 0 (param-space loads miss)
+    P.j = a.cta_j0[cta_slot(a)];  // g >= this CTA's first item: no scan from job 0 (param-space loads miss)
     while (P.j + 1 < a.n_jobs && a.jobs[P.j + 1].ibase <= g) ++P.j;
     const Job& J = a.jobs[P.j];
     P.s = (g - J.ibase) / J.NRT;
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     };
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = blockIdx.x, G = gridDim.x;
+    const int b = cta_slot(a), G = gridDim.x;
     if (warp == 0) ABCQ_BTRACE(0);
     uint64_t* mybar = bars + warp * R;
     if (lane == 0) {

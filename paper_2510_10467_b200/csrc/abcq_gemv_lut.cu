@@ -208,7 +208,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             }
     }
     a.prefill = g_prefill;
-    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22 || g_dbg_mode == 29 || g_dbg_mode == 32) ? g_dbg_mode : 0;
+    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22 || g_dbg_mode == 29 || g_dbg_mode == 32 || g_dbg_mode == 33) ? g_dbg_mode : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
     // round trace: after the 16 launch slots, [warp][round < 32][4] stamps of CTA g_rtrace_cta

@@ -165,6 +165,18 @@ int abcq_gemv_add_rmsnorm(const abcq_model_t* m, int32_t p, const void* d_x, con
                           const void* d_norm_w, float eps, void* d_x_out, void* d_y, int32_t y_dtype,
                           void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Decoder output fusion (the Llama-3 decode harness): y = W x
+ * at precision p (f16 y; x f16 or ABCQ_F16_SILU_GLU), then -- in the block
+ * that completes the split-K sums last -- stream += y and
+ * h = rmsnorm(stream) * norm_w with abcq_add_rmsnorm_f16's arithmetic
+ * (bitwise equal to y = abcq_gemv; abcq_add_rmsnorm_f16(stream, y, norm_w, h)),
+ * one launch instead of two. The persistent kernel always (never the cluster
+ * kernel); rows <= 8192, cols > 256, y / stream / h distinct; workspace as
+ * abcq_gemv. */
+int abcq_gemv_rmsnorm_out(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
+                          void* d_stream, const void* d_norm_w, float eps, void* d_h, void* d_workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* ---- batches of independent GEMVs ----------------------------------------
  * One persistent launch runs n_jobs GemvEngine.lut calls back to back (the
  * TMA stream never drains between them) -- e.g. q/k/v or gate/up of a

@@ -226,6 +226,25 @@ int abcq_gemv_add_rmsnorm(const abcq_model_t* m, int32_t p, const void* d_x, con
                     "abcq_gemv_add_rmsnorm");
 }
 
+int abcq_gemv_rmsnorm_out(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
+                          void* d_stream, const void* d_norm_w, float eps, void* d_h, void* d_workspace,
+                          size_t workspace_bytes, void* stream) {
+    if (int rc = check_call(m, p, d_x, x_dtype, d_y, ABCQ_F16)) return rc;
+    if (!abcq::lut_supports(m, p)) return fail(ABCQ_E_LAYOUT, "abcq_gemv_rmsnorm_out needs the tiled layout (group 128)");
+    if (x_dtype == ABCQ_F32) return fail(ABCQ_E_ARG, "abcq_gemv_rmsnorm_out: x must be f16 (or f16 SiLU-gated)");
+    if (!d_stream || !d_norm_w || !d_h) return fail(ABCQ_E_ARG, "abcq_gemv_rmsnorm_out: stream / norm_w / h is NULL");
+    if (m->rows > abcq::kRmsMaxN) return fail(ABCQ_E_ARG, "abcq_gemv_rmsnorm_out: rows %d > %d", m->rows, abcq::kRmsMaxN);
+    if (m->cols <= 256) return fail(ABCQ_E_ARG, "abcq_gemv_rmsnorm_out: cols %d <= 256 (no split-K completion)", m->cols);
+    if (d_h == d_stream || d_h == d_y || d_stream == d_y)
+        return fail(ABCQ_E_ARG, "abcq_gemv_rmsnorm_out: y, stream and h must be distinct buffers");
+    const size_t need = abcq::lut_workspace_bytes(m);
+    if (need && (!d_workspace || workspace_bytes < need))
+        return fail(ABCQ_E_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+    abcq::NormOut nout{d_stream, d_norm_w, d_h, eps};
+    return cuda_ret(abcq::launch_gemv_rmsnorm_out(m, p, d_x, x_dtype, d_y, nout, d_workspace, (cudaStream_t)stream),
+                    "abcq_gemv_rmsnorm_out");
+}
+
 int abcq_gemv_batch_max_jobs(void) { return abcq::lut_max_jobs(); }
 
 static int check_jobs(const abcq_gemv_job_t* jobs, int32_t n) {

@@ -41,6 +41,10 @@ struct Job {
     const __half* nw;   // RMSNorm weight
     __half* xo;         // x + res written back (the residual stream; may be NULL)
     float eps;
+    __half* ep_x;        // norm epilogue (abcq_gemv_rmsnorm_out; single split f16 jobs): residual stream, += y
+    const __half* ep_w;  // RMSNorm weight
+    __half* ep_h;        // rmsnorm(stream) * w
+    float ep_eps;
     uint32_t* arrive;   // CTAs done streaming this job (split jobs; self-resetting)
     uint32_t* reduced;  // reduce blocks done with this job (self-resetting)
     int ncta;           // CTAs whose range touches this job
@@ -256,7 +260,7 @@ constexpr int kReduceRows = kReduceThreads / kReduceTPR * kReduceRPT;  // rows p
 // not earlier, or the next kernel's CTAs take the SMs that the remaining
 // reduce blocks of this grid still need.
 template <int NJ, typename YT, int RPB, int RPT, bool RELEASE, bool PRE_WAIT = false>
-__device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
+__device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
     constexpr int rpb = RPB;
     // blocks laid out job by job, jobs of more than 16 slices first: their
     // completion is the longest, and the blocks reach SMs in index order as
@@ -277,7 +281,7 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
     if (j < 0) {
         if (PRE_WAIT) pdl_wait();
         if (RELEASE) pdl_launch_dependents();
-        return;
+        return -1;
     }
     const Job& J = a.jobs[j];
     if (PRE_WAIT) pdl_wait();  // (after the param-space job scan: y may still be read by the previous kernel)
@@ -340,6 +344,7 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
         for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
         if (sub == 0 && row[q] < J.rows) static_cast<YT*>(J.y)[row[q]] = from_f32<YT>(tot);
     }
+    if (J.ep_x) __threadfence();  // release the y rows to the block that runs the norm epilogue
     __syncthreads();
     if (threadIdx.x == 0) {
         if (a.trace) {  // profiling: last block end, per job
@@ -347,9 +352,35 @@ __device__ __forceinline__ void reduce_rows(const KArgs<NJ>& a, int blk) {
             atomicMax(&a.trace[148 * 8 + 2], t);
             if (j < 32) atomicMax(&a.trace[149 * 8 + j], t);
         }
-        if (atomicAdd(J.reduced, 1u) == (uint32_t)(nbj - 1)) {  // last block of job j: recycle
+    }
+    // (the job's norm epilogue, if any, runs in the block that completes it last)
+    bool last = false;
+    if (threadIdx.x == 0) {
+        last = atomicAdd(J.reduced, 1u) == (uint32_t)(nbj - 1);
+        if (last) {  // last block of job j: recycle
             *J.arrive = 0u;
             *J.reduced = 0u;
+        }
+    }
+    if (J.ep_x) return __syncthreads_or(last) ? j : -1;  // (block-uniform: a parameter)
+    return -1;
+}
+
+// norm epilogue of job J (the block that completed its split-K sums last,
+// 512 threads): stream += y; h = rmsnorm(stream) * w -- add_rmsnorm_kernel's
+// arithmetic through the same helpers, so bitwise equal to that launch
+__device__ __forceinline__ void rmsnorm_epilogue(const Job& J, float* red) {
+    __threadfence();  // acquire: every completion block's y rows
+    float v[16];
+    const int t = threadIdx.x;
+    const float ss = rms_load(J.ep_x, static_cast<const __half*>(J.y), J.rows, t, v);
+    const float inv = rms_inv(ss, J.rows, J.ep_eps, red);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int i = (k < 8 ? 8 * t + k : 4096 + 8 * t + (k - 8));
+        if (i < J.rows) {
+            J.ep_x[i] = __float2half_rn(v[k]);
+            J.ep_h[i] = __float2half_rn(v[k] * inv * __half2float(J.ep_w[i]));
         }
     }
 }
@@ -374,7 +405,11 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             // retire) -- for batches whose reduce fits one wave; larger ones
             // use the separate kernel (a trailing CTA needs a whole SM, and
             // the role's code in the kernel costs the streams ~7%)
-            reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true, true>(a, blockIdx.x - a.main_ctas);
+            const int ej = reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true, true>(a, blockIdx.x - a.main_ctas);
+            if constexpr (std::is_same<YT, __half>::value) {
+                extern __shared__ __align__(1024) char ep_smem[];
+                if (ej >= 0) rmsnorm_epilogue(a.jobs[ej], reinterpret_cast<float*>(ep_smem));
+            }
             return;
         }
     }
@@ -834,6 +869,8 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kFusedRows - 1) / kFusedRows;
     constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
     const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
+    if (ba.jobs[0].ep_x && (!fused || ba.n_jobs != 1 || ba.jobs[0].NS <= 1 || !std::is_same<YT, __half>::value))
+        return (int)cudaErrorInvalidConfiguration;  // the norm epilogue runs in the trailing completion CTAs
     auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse> : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>;
     constexpr int smem = SlotGeom<ST, ASYM>::kSmem;
     static_assert(smem <= 227 * 1024, "shared memory budget");

@@ -65,6 +65,10 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.nw = nullptr;
     J.xo = nullptr;
     J.eps = 0.f;
+    J.ep_x = nullptr;
+    J.ep_w = nullptr;
+    J.ep_h = nullptr;
+    J.ep_eps = 0.f;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
     J.ncta = 0;
@@ -77,7 +81,8 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 }
 
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin) {
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin,
+                     const NormOut* nout) {
     BatchArgs a;  // passed by value (kernel parameter space)
     const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
     // fixed cost of a (job, slice) piece in blocks: measured best 300 for
@@ -99,6 +104,12 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             a.jobs[0].nw = static_cast<const __half*>(nin->norm_w);
             a.jobs[0].xo = static_cast<__half*>(nin->x_out);
             a.jobs[0].eps = nin->eps;
+        }
+        if (nout && j == 0) {
+            a.jobs[0].ep_x = static_cast<__half*>(nout->stream);
+            a.jobs[0].ep_w = static_cast<const __half*>(nout->norm_w);
+            a.jobs[0].ep_h = static_cast<__half*>(nout->h);
+            a.jobs[0].ep_eps = nout->eps;
         }
         w += partial_bytes(models[j]);
         a.jobs[j].arrive = counters ? counters + j * kCounterStride : nullptr;
@@ -230,6 +241,11 @@ int launch_gemv_add_rmsnorm(const abcq_model_t* m, int p, const NormIn& nin, voi
     const int xd = ABCQ_F16;
     const void* x = nin.x;
     return launch_gemv_jobs(&m, &p, &x, &y, 1, &xd, y_dtype, ws, st, &nin);
+}
+
+int launch_gemv_rmsnorm_out(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, const NormOut& nout,
+                            void* ws, cudaStream_t st) {
+    return launch_gemv_jobs(&m, &p, &x, &y, 1, &x_dtype, ABCQ_F16, ws, st, nullptr, &nout);
 }
 
 }  // namespace abcq

@@ -26,8 +26,10 @@ int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, vo
 // batch of n independent GEMVs (same dtypes / mode), workspaces concatenated
 // in job order (lut_workspace_bytes each)
 struct NormIn;
+struct NormOut;
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
-                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin = nullptr);
+                     int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin = nullptr,
+                     const NormOut* nout = nullptr);
 int lut_max_jobs();
 
 // fused input mode of the persistent GEMV: input = f16(f16(x + residual) * inv_rms * norm_w),
@@ -41,6 +43,17 @@ struct NormIn {
 };
 int launch_gemv_add_rmsnorm(const abcq_model_t* m, int p, const NormIn& nin, void* y, int y_dtype, void* ws,
                             cudaStream_t st);
+// fused output mode (norm epilogue): after y = W x (f16), the last split-K
+// completion CTA does stream += y; h = rmsnorm(stream) * norm_w
+// (add_rmsnorm_kernel's arithmetic, bitwise)
+struct NormOut {
+    void* stream;  // residual stream (f16, updated in place)
+    const void* norm_w;
+    void* h;
+    float eps;
+};
+int launch_gemv_rmsnorm_out(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, const NormOut& nout,
+                            void* ws, cudaStream_t st);
 
 // single GEMV through the cluster kernel (abcq_gemv_cluster.cu): no workspace
 bool cluster_supports(const abcq_model_t* m, int p);

@@ -153,8 +153,19 @@ class QuantizedLlamaStep:
 
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), p: int = 3, p_lo: int = 2, p_hi: int = 4,
                  ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True, stack_rows: bool = True,
-                 fuse_norm: bool = False):
+                 fuse_norm: bool = False, fuse_norm_out: bool = False):
         self.cfg, self.p, self.fuse_glu, self.stack_rows = cfg, p, fuse_glu, stack_rows
+        # fuse_norm_out: the add + RMSNorm after the o and down projections runs
+        # as those GEMVs' epilogue (abcq_gemv_rmsnorm_out: the block that
+        # completes the split-K sums last does stream += y; h = rmsnorm(stream)
+        # * w, bitwise equal to the separate launch) -- two launches fewer per
+        # layer, but measured slower: p3 2.37 vs 2.25 ms/token (the one-CTA
+        # epilogue serialises at the grid's tail, where the separate 1-block
+        # launch ran while the next GEMV's CTAs were already prefetching;
+        # tools/decode_norm_out_ab.py), so off by default
+        if fuse_norm and fuse_norm_out:
+            raise ValueError("fuse_norm (GEMV input side) and fuse_norm_out (output side) are exclusive")
+        self.fuse_norm_out = fuse_norm_out and fuse_glu and stack_rows
         # fuse_norm: add + RMSNorm formed inside the q/k/v and gate/up GEMVs'
         # table builds (abcq_gemv_add_rmsnorm, bitwise equal to the separate
         # launch). Off by default: measured 2.14 vs 2.11 ms/token at p=3 -- every
@@ -225,6 +236,8 @@ class QuantizedLlamaStep:
         return cur
 
     def step(self):
+        if self.fuse_norm_out:
+            return self._step_norm_out()
         cfg, p = self.cfg, self.p
         resid = None
         cur, nxt = self.x, self.x_alt  # an even number of fused norms per step: it ends in self.x
@@ -250,6 +263,33 @@ class QuantizedLlamaStep:
         add_rmsnorm(self.x, resid, self.final_norm, self.h, cfg.eps)
         torch.mv(self.lm_head, self.h, out=self.logits)
         return self.argmax(self.logits, self.token)
+
+    def _step_norm_out(self):
+        """The step with every add+RMSNorm but the first fused into the GEMV
+        before it: o -> (x += o; h = norm2(x)), down -> (x += d; h = norm1 of
+        the next layer, or the final norm). Same arithmetic as step()."""
+        cfg, p = self.cfg, self.p
+        n = len(self.layers)
+        add_rmsnorm(self.x, None, self.norm_w[0][0], self.h, cfg.eps)
+        for li, mats in enumerate(self.layers):
+            _persistent(mats["qkv"], p, self.h, self.qkv)
+            a = self.attn(li, self.q, self.k, self.v)
+            _norm_out(mats["o"], p, a, self.o, self.x, self.norm_w[li][1], cfg.eps, self.h)
+            mats["gu"].gemv(p, self.h, out=self.gu)
+            w_next = self.norm_w[li + 1][0] if li + 1 < n else self.final_norm
+            _norm_out(mats["down"], p, self.gu, self.d, self.x, w_next, cfg.eps, self.h, silu_glu=True)
+        torch.mv(self.lm_head, self.h, out=self.logits)
+        return self.argmax(self.logits, self.token)
+
+
+def _norm_out(m, p, x, out, stream, w, eps, h, silu_glu=False):
+    """out = W x, then stream += out; h = rmsnorm(stream) * w -- one launch for a
+    DeviceModel (its norm epilogue), else the GEMV and the separate launch."""
+    if isinstance(m, DeviceModel):
+        m.gemv_rmsnorm_out(p, x, out, stream, w, eps, h, silu_glu=silu_glu)
+    else:
+        m.gemv(p, x, out=out, silu_glu=silu_glu) if silu_glu else m.gemv(p, x, out=out)
+        add_rmsnorm(stream, out, w, h, eps)
 
 
 class Fp16LlamaStep:

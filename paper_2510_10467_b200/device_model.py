@@ -286,6 +286,29 @@ class DeviceModel:
             "abcq_gemv_add_rmsnorm")
         return out
 
+    def gemv_rmsnorm_out(self, p: int, x: torch.Tensor, out: torch.Tensor, resid_stream: torch.Tensor,
+                         norm_w: torch.Tensor, eps: float, h: torch.Tensor, silu_glu: bool = False,
+                         stream=None) -> torch.Tensor:
+        """out = W_p x (f16), then resid_stream += out and h = rmsnorm(resid_stream)
+        * norm_w in the same launch (the decoder's next add+RMSNorm as the GEMV's
+        epilogue; abcq_gemv_rmsnorm_out, bitwise equal to gemv + add_rmsnorm).
+        x: f16 (cols,) or, with silu_glu, the (2*cols,) [gate ; up] buffer;
+        out / resid_stream / norm_w / h: distinct contiguous f16 (rows,) tensors."""
+        self._check_p(p)
+        want = 2 * self.cols if silu_glu else self.cols
+        if x.dtype != torch.float16 or x.numel() != want or x.device != self.device or not x.is_contiguous():
+            raise UsageError(f"x must be a contiguous f16 tensor of {want} elements")
+        for t in (out, resid_stream, norm_w, h):
+            if t.dtype != torch.float16 or t.numel() != self.rows or t.device != self.device or not t.is_contiguous():
+                raise UsageError("out / resid_stream / norm_w / h must be contiguous f16 tensors of `rows` elements")
+        self._order_after_upload(p, stream)
+        ws = self.workspace(stream)
+        xd = _lib.F16_SILU_GLU if silu_glu else dtype_code(torch.float16)
+        _lib.check(_lib.lib().abcq_gemv_rmsnorm_out(
+            self.struct_ptr(), p, x.data_ptr(), xd, out.data_ptr(), resid_stream.data_ptr(), norm_w.data_ptr(),
+            float(eps), h.data_ptr(), ws.data_ptr(), ws.numel(), _stream_handle(stream)), "abcq_gemv_rmsnorm_out")
+        return out
+
     def gemm_mixedp(self, ps, X: torch.Tensor, out_dtype=torch.float32, stream=None) -> torch.Tensor:
         """Y[b] = W_{ps[b]} X[b] for B <= 16 requests in one pass over the planes
         (tensor cores). X: (B, cols) CUDA tensor (cast to fp16); returns (B, rows)."""

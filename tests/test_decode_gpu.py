@@ -268,3 +268,72 @@ def test_gemv_add_rmsnorm_matches_separate_ops():
         assert torch.equal(xo, xs)
     with pytest.raises(P.UsageError):
         dm.gemv_add_rmsnorm(3, x, r, w, 1e-5, out=y, x_out=x)   # x_out aliases x
+
+
+def test_quantized_step_norm_out_equals_separate_add_rmsnorm():
+    """add + RMSNorm as the o / down GEMVs' epilogue (abcq_gemv_rmsnorm_out,
+    fuse_norm_out=True) == the separate launches: bitwise equal step state and token."""
+    from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    cfg = LlamaConfig(layers=3, vocab=1000)
+    m = QuantizedLlamaStep(cfg, p=3, ctx=64, fuse_norm_out=True)
+    assert m.fuse_norm_out
+    x0 = m.x.clone()
+    k0, v0 = m.attn.k_cache.clone(), m.attn.v_cache.clone()
+    t1 = m.step().item()
+    x1, h1, gu1, qkv1, lg1 = m.x.clone(), m.h.clone(), m.gu.clone(), m.qkv.clone(), m.logits.clone()
+    m.x.copy_(x0)
+    m.attn.k_cache.copy_(k0)
+    m.attn.v_cache.copy_(v0)
+    m.fuse_norm_out = False
+    t2 = m.step().item()
+    assert t1 == t2
+    for a, b in ((m.x, x1), (m.h, h1), (m.gu, gu1), (m.qkv, qkv1), (m.logits, lg1)):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("rows,cols,glu", [(4096, 4096, False), (4096, 14336, True), (8192, 1024, False)])
+def test_gemv_rmsnorm_out_matches_separate_ops(rows, cols, glu):
+    """The norm epilogue vs the persistent GEMV + add_rmsnorm launch (both
+    bitwise): y, the updated residual stream and h; plus the usage checks."""
+    import paper_2510_10467_b200 as P
+    from paper_2510_10467_b200.decode import add_rmsnorm
+    dm = P.DeviceModel(rows, cols, 128, 2, 4, scale_dtype="f16")
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, rows, cols // 32), dtype=torch.int32, device="cuda",
+                                 generator=g))
+    for q in (2, 3, 4):
+        dm.load_scale_set(q, (0.01 + 0.01 * torch.rand((q, rows, cols // 128), device="cuda", generator=g)) / 4)
+    x = torch.randn(2 * cols if glu else cols, device="cuda", generator=g).half()
+    s0 = torch.randn(rows, device="cuda", generator=g).half()
+    w = (1 + 0.1 * torch.randn(rows, device="cuda", generator=g)).half()
+    for p in (2, 4):
+        y, st, h = torch.empty_like(s0), s0.clone(), torch.empty_like(s0)
+        for _ in range(2):  # twice: the self-resetting counters
+            st.copy_(s0)
+            dm.gemv_rmsnorm_out(p, x, y, st, w, 1e-5, h, silu_glu=glu)
+        ref_y = torch.empty_like(y)
+        _batch_one(dm, p, x, ref_y, glu)
+        st_ref, h_ref = s0.clone(), torch.empty_like(s0)
+        add_rmsnorm(st_ref, ref_y, w, h_ref, 1e-5)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref_y), p
+        assert torch.equal(st, st_ref) and torch.equal(h, h_ref), p
+    with pytest.raises(P.UsageError):
+        dm.gemv_rmsnorm_out(2, x, y, y, w, 1e-5, h, silu_glu=glu)  # stream aliases y
+
+
+def _batch_one(dm, p, x, y, glu):
+    """y = W_p x through the persistent batch kernel (a batch of one job)."""
+    import ctypes as C
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.device_model import dtype_code
+    job = _lib.AbcqGemvJob()
+    job.model = C.pointer(dm._struct)
+    job.p = p
+    job.x_dtype = _lib.F16_SILU_GLU if glu else dtype_code(x.dtype)
+    job.y_dtype = dtype_code(y.dtype)
+    job.x = x.data_ptr()
+    job.y = y.data_ptr()
+    ws = dm.workspace(None)
+    _lib.check(_lib.lib().abcq_gemv_batch(C.byref(job), 1, ws.data_ptr(), ws.numel(),
+                                           torch.cuda.current_stream().cuda_stream), "abcq_gemv_batch")

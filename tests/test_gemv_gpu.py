@@ -472,6 +472,38 @@ def test_split_k_completion_paths_agree(P):
         assert torch.equal(o, f)
 
 
+@pytest.mark.parametrize("asym", [False, True])
+def test_batch_schedule_variants_bitwise_equal(P, asym):
+    """The schedule only decides which warp / CTA / completion block does an
+    item, never the arithmetic: the slot-sized chunk split of multi-round CTAs
+    vs the round-1 cost split (debug mode 32), the completion blocks of >16-slice
+    jobs first vs job order (29), the schedule reversed over the CTAs (33) --
+    bitwise equal y, over a batch of many short pieces (k/v-sized jobs at
+    several precisions, a 56-slice job)."""
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.device_model import gemv_batch
+    shapes = [(1024, 4096), (4096, 4096), (512, 14336), (2000, 1000), (16, 4096)]
+    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 1, 4, asym=asym, seed=r + c), scale_dtype="f16")
+           for r, c in shapes]
+    x = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for _, c in shapes}
+    jobs = [(dm, p, x[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16))
+            for p in (1, 2, 3, 4) for dm in dms]
+    gemv_batch(jobs)
+    torch.cuda.synchronize()
+    base = [o.clone() for *_, o in jobs]
+    for mode in (32, 29, 33):
+        _lib.lib().abcq_debug_set_mode(mode)
+        try:
+            for o in (j[3] for j in jobs):
+                o.fill_(0)
+            gemv_batch(jobs)
+            torch.cuda.synchronize()
+        finally:
+            _lib.lib().abcq_debug_set_mode(0)
+        for (dm, p, _, o), b in zip(jobs, base):
+            assert torch.equal(o, b), (mode, dm.rows, dm.cols, p)
+
+
 def test_gemv_batch_asymmetric(P):
     from paper_2510_10467_b200.device_model import gemv_batch
     ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]

@@ -58,6 +58,7 @@ STEP_GROUPS = [tuple(range(7))]
 DECODER_GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
 E2E_GROUP = 4     # e2e steps per copy-pipeline group
+MP_RESERVE_SMS = 4  # N > 1: SMs left to the overlapping NCCL all-gather (abcq_set_reserved_sms, NCCL_MAX_CTAS)
 P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
 XY_BYTES = 2      # fp16 x and y
@@ -298,11 +299,23 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     mp = world > 1 or os.environ.get("ABCQ_BENCH_FORCE_MP") == "1"
+    mp_reserve = 0
     if mp:
+        # the step's all-gather runs beside the next step's GEMV (another
+        # stream): NCCL is capped at MP_RESERVE_SMS CTAs and the persistent
+        # GEMV grid leaves that many SMs free, so neither waits for the
+        # other's SMs (at world size 1 -- the forced-MP test -- the gather is a
+        # local copy and the reserve only costs: 4.61 vs 4.68 TB/s)
+        mp_reserve = int(os.environ.get("ABCQ_BENCH_MP_RESERVE", str(MP_RESERVE_SMS if world > 1 else 0)))
+        if mp_reserve:
+            os.environ.setdefault("NCCL_MAX_CTAS", str(mp_reserve))
+            os.environ.setdefault("NCCL_MIN_CTAS", "1")
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(device=dev)
     ctx = Ctx(dev, stream, rank, world)
     P, gemv_batch = ctx.P, ctx.gemv_batch
+    if mp_reserve:
+        P.set_reserved_sms(mp_reserve)
 
     copies = len(PRECISIONS)
     models, host = make_layer_models(P, 1, copies, seed0=17 * rank, keep_host=(rank == 0))
@@ -494,6 +507,8 @@ def run_gpu(args):
                                   "step's GEMV (double-buffered), CUDA events, max over ranks"
                                   if use_graph else graph_mode + ": one NCCL all-gather of the step's 21 outputs "
                                   "per step overlapping the next step (double-buffered), CUDA events, max over ranks"))
+        if mp_reserve:
+            timing += f"; the GEMV grid leaves {mp_reserve} SMs to the all-gather (NCCL_MAX_CTAS={mp_reserve})"
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),

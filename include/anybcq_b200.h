@@ -88,6 +88,14 @@ const char* abcq_last_error(void);
 /* 0 if device `dev` is sm_100 and the sm_100a kernels load, else ABCQ_E_DEVICE */
 int abcq_device_check(int32_t dev);
 
+/* The persistent GEMV grid takes one CTA per SM (whole SMs: 227 KB of shared
+ * memory, all registers). A kernel running BESIDE it on another stream (an
+ * NCCL collective overlapping the GEMV) would hold SMs that some of its CTAs
+ * then wait for; n > 0 sizes later persistent grids to (SMs - n), leaving n
+ * SMs free. Process-wide (all devices); default 0; *prev_out (if not NULL)
+ * receives the previous value. ABCQ_E_ARG for n outside [0, SMs).          */
+int abcq_set_reserved_sms(int32_t n, int32_t* prev_out);
+
 /* profiling aid: when d_buf != NULL, every later LUT GEMV launch writes 8
  * u64 %globaltimer stamps per CTA (phases: start, prefetch issued, PDL wait
  * done, table built, stream done, reduction done) to d_buf[cta*8 + k].    */

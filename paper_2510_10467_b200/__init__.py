@@ -20,7 +20,7 @@ def __getattr__(name):
                 "render_bench_csv"):
         from . import engine
         return getattr(engine, name)
-    if name in ("DeviceModel", "GemvBatchPlan", "gemv_batch"):
+    if name in ("DeviceModel", "GemvBatchPlan", "gemv_batch", "set_reserved_sms"):
         from . import device_model
         return getattr(device_model, name)
     if name in ("QuantizedMatrix", "greedy_init", "ls_update_scales", "bs_recalibrate_codes", "alternate_fit",

@@ -67,6 +67,7 @@ SIGNATURES = {
     "abcq_last_error": (C.c_char_p, []),
     "abcq_device_check": (C.c_int, [_i32]),
     "abcq_debug_set_trace": (C.c_int, [_vp]),
+    "abcq_set_reserved_sms": (C.c_int, [_i32, C.POINTER(C.c_int32)]),
     "abcq_debug_set_mode": (C.c_int, [_i32]),
     "abcq_debug_gemv_geometry": (C.c_int, [_PM, _i32, C.POINTER(_i32)]),
     "abcq_argmax_workspace_bytes": (C.c_int, [C.POINTER(_sz)]),

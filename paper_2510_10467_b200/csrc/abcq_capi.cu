@@ -76,6 +76,13 @@ extern "C" {
 
 int abcq_abi_version(void) { return ABCQ_ABI_VERSION; }
 
+int abcq_set_reserved_sms(int32_t n, int32_t* prev_out) {
+    if (n < 0 || n >= abcq::num_sms()) return fail(ABCQ_E_ARG, "reserved SMs %d outside [0, %d)", n, abcq::num_sms());
+    if (prev_out) *prev_out = abcq::g_reserved_sms;
+    abcq::g_reserved_sms = n;
+    return 0;
+}
+
 int abcq_debug_set_mode(int32_t mode) {
     if (mode >= 7000 && mode < 7000 + 1 + 255) {  // batch kernel round trace of CTA mode - 7001 (7000 = off)
         abcq::g_rtrace_cta = mode - 7001;

@@ -16,7 +16,8 @@ int g_dbg_mode = 0;                     // abcq_debug_set_mode (profiling experi
 // fixed cost of a (job, slice) piece in 512-byte blocks (load-balance model;
 // abcq_debug_set_mode(1000 + v) sets it to v)
 int g_piece_blocks = 0;  // 0: by batch size (below)
-int g_partition = 0;  // 0: greedy fill with exact piece costs; 1: proportional (abcq_debug_set_mode(3000 + v))
+int g_partition = 0;
+int g_reserved_sms = 0;  // abcq_set_reserved_sms: SMs the persistent grid leaves to concurrent kernels  // 0: greedy fill with exact piece costs; 1: proportional (abcq_debug_set_mode(3000 + v))
 int g_prefill = 8;  // ring slots issued before the PDL wait (all of them); abcq_debug_set_mode(2000 + v)
 constexpr int kCostScale = 64;
 
@@ -84,7 +85,10 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
                      int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin,
                      const NormOut* nout) {
     BatchArgs a;  // passed by value (kernel parameter space)
-    const int grid = num_sms() < kMaxGrid ? num_sms() : kMaxGrid;
+    // one CTA per SM, minus the SMs reserved for kernels that run beside the
+    // GEMV (e.g. an NCCL collective on another stream overlapping it)
+    int grid = num_sms() - g_reserved_sms;
+    grid = grid < 1 ? 1 : (grid > kMaxGrid ? kMaxGrid : grid);
     // fixed cost of a (job, slice) piece in blocks: measured best 300 for
     // single GEMVs and decoder-sized groups, 130-160 for large batches (bench
     // step 60.4 -> 59.6 us; tools/ab_step.py / ab_small.py with modes 1xxx)

@@ -105,6 +105,7 @@ extern int g_dbg_mode;
 extern int g_piece_blocks;
 extern int g_prefill;
 extern int g_partition;
+extern int g_reserved_sms;
 int num_sms();
 int probe_kernel_image();  // cudaFuncGetAttributes on a packing kernel
 

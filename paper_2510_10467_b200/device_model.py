@@ -485,3 +485,12 @@ class GemvBatchPlan:
             ws = self._ws[sh] = torch.zeros(self.need, dtype=torch.uint8, device=self.device)
         _lib.check(self._L.abcq_gemv_batch(self.arr, self.n, ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch")
         return [j[3] for j in self.jobs]
+
+
+def set_reserved_sms(n: int) -> int:
+    """Leave n SMs free of later persistent GEMV grids (for a kernel that runs
+    beside them on another stream, e.g. an NCCL all-gather overlapping the
+    next GEMV; abcq_set_reserved_sms). Returns the previous value."""
+    prev = C.c_int32()
+    _lib.check(_lib.lib().abcq_set_reserved_sms(int(n), C.byref(prev)), "abcq_set_reserved_sms")
+    return int(prev.value)

@@ -504,6 +504,30 @@ def test_batch_schedule_variants_bitwise_equal(P, asym):
             assert torch.equal(o, b), (mode, dm.rows, dm.cols, p)
 
 
+def test_reserved_sms_same_results(P):
+    """abcq_set_reserved_sms: a smaller persistent grid (SMs left to a kernel
+    running beside it) changes only the schedule -- bitwise equal y; the
+    bound check is a usage error."""
+    from paper_2510_10467_b200.device_model import gemv_batch, set_reserved_sms
+    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r + c), scale_dtype="f16")
+           for r, c in ((4096, 4096), (1024, 14336))]
+    x = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for c in (4096, 14336)}
+    jobs = [(dm, p, x[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16)) for dm in dms for p in (2, 4)]
+    gemv_batch(jobs)
+    torch.cuda.synchronize()
+    base = [o.clone() for *_, o in jobs]
+    try:
+        assert set_reserved_sms(20) == 0
+        gemv_batch(jobs)
+        torch.cuda.synchronize()
+        with pytest.raises(P.UsageError):
+            set_reserved_sms(100000)
+    finally:
+        assert set_reserved_sms(0) == 20
+    for (*_, o), b in zip(jobs, base):
+        assert torch.equal(o, b)
+
+
 def test_gemv_batch_asymmetric(P):
     from paper_2510_10467_b200.device_model import gemv_batch
     ms = [P.DeviceModel.from_model(synth_model(P, r, 1024, 2, 3, asym=True, seed=r)) for r in (128, 300)]

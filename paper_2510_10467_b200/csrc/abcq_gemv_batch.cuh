@@ -41,16 +41,21 @@ struct Job {
     const __half* nw;   // RMSNorm weight
     __half* xo;         // x + res written back (the residual stream; may be NULL)
     float eps;
-    __half* ep_x;        // norm epilogue (abcq_gemv_rmsnorm_out; single split f16 jobs): residual stream, += y
-    const __half* ep_w;  // RMSNorm weight
-    __half* ep_h;        // rmsnorm(stream) * w
-    float ep_eps;
     uint32_t* arrive;   // CTAs done streaming this job (split jobs; self-resetting)
     uint32_t* reduced;  // reduce blocks done with this job (self-resetting)
     int ncta;           // CTAs whose range touches this job
     int ibase;      // first item of this job in the batch's item sequence
     int w;          // cost units per item: p blocks + the item's share of a table build
     int64_t ubase;  // first cost unit of this job (sum of items * w before it)
+};
+
+// norm epilogue (abcq_gemv_rmsnorm_out; a single split job with f16 y):
+// stream += y; h = rmsnorm(stream) * w in the block completing the job last
+struct Epi {
+    __half* x;        // residual stream (updated in place); NULL: no epilogue
+    const __half* w;  // RMSNorm weight
+    __half* h;
+    float eps;
 };
 
 // kernel parameter: NJ job slots (1, 8 or 32 -- the smallest that fits)
@@ -71,6 +76,7 @@ struct KArgs {
     unsigned long long* trace;
     unsigned long long* rtrace;  // per-warp round stamps of CTA rtrace_cta (profiling), or NULL
     int rtrace_cta;
+    Epi ep;                      // norm epilogue of job 0 (abcq_gemv_rmsnorm_out), ep.x == NULL: none
 };
 
 struct BatchArgs {
@@ -87,6 +93,7 @@ struct BatchArgs {
     unsigned long long* trace;  // optional per-CTA stamps (abcq_debug_set_trace)
     unsigned long long* rtrace;
     int rtrace_cta;
+    Epi ep;
 };
 
 template <typename ST, bool ASYM>
@@ -344,7 +351,8 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
         for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
         if (sub == 0 && row[q] < J.rows) static_cast<YT*>(J.y)[row[q]] = from_f32<YT>(tot);
     }
-    if (J.ep_x) __threadfence();  // release the y rows to the block that runs the norm epilogue
+    const bool epi = j == 0 && a.ep.x != nullptr;
+    if (epi) __threadfence();  // release the y rows to the block that runs the norm epilogue
     __syncthreads();
     if (threadIdx.x == 0) {
         if (a.trace) {  // profiling: last block end, per job
@@ -362,25 +370,25 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
             *J.reduced = 0u;
         }
     }
-    if (J.ep_x) return __syncthreads_or(last) ? j : -1;  // (block-uniform: a parameter)
+    if (epi) return __syncthreads_or(last) ? j : -1;  // (block-uniform)
     return -1;
 }
 
 // norm epilogue of job J (the block that completed its split-K sums last,
 // 512 threads): stream += y; h = rmsnorm(stream) * w -- add_rmsnorm_kernel's
 // arithmetic through the same helpers, so bitwise equal to that launch
-__device__ __forceinline__ void rmsnorm_epilogue(const Job& J, float* red) {
+__device__ __forceinline__ void rmsnorm_epilogue(const Job& J, const Epi& E, float* red) {
     __threadfence();  // acquire: every completion block's y rows
     float v[16];
     const int t = threadIdx.x;
-    const float ss = rms_load(J.ep_x, static_cast<const __half*>(J.y), J.rows, t, v);
-    const float inv = rms_inv(ss, J.rows, J.ep_eps, red);
+    const float ss = rms_load(E.x, static_cast<const __half*>(J.y), J.rows, t, v);
+    const float inv = rms_inv(ss, J.rows, E.eps, red);
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         const int i = (k < 8 ? 8 * t + k : 4096 + 8 * t + (k - 8));
         if (i < J.rows) {
-            J.ep_x[i] = __float2half_rn(v[k]);
-            J.ep_h[i] = __float2half_rn(v[k] * inv * __half2float(J.ep_w[i]));
+            E.x[i] = __float2half_rn(v[k]);
+            E.h[i] = __float2half_rn(v[k] * inv * __half2float(E.w[i]));
         }
     }
 }
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
             const int ej = reduce_rows<NJ, YT, kBThreads / kReduceTPR, 1, true, true>(a, blockIdx.x - a.main_ctas);
             if constexpr (std::is_same<YT, __half>::value) {
                 extern __shared__ __align__(1024) char ep_smem[];
-                if (ej >= 0) rmsnorm_epilogue(a.jobs[ej], reinterpret_cast<float*>(ep_smem));
+                if (ej >= 0) rmsnorm_epilogue(a.jobs[ej], a.ep, reinterpret_cast<float*>(ep_smem));
             }
             return;
         }
@@ -863,13 +871,14 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     a.trace = ba.trace;
     a.rtrace = ba.rtrace;
     a.rtrace_cta = ba.rtrace_cta;
+    a.ep = ba.ep;
     int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/4) per job)
     constexpr int kFusedRows = kBThreads / kReduceTPR;
     for (int j = 0; j < ba.n_jobs; ++j)
         if (ba.jobs[j].NS > 1) rblocks += (ba.jobs[j].rows + kFusedRows - 1) / kFusedRows;
     constexpr bool kCanFuse = NJ <= 8;  // fused variant instantiated for single GEMVs and small batches
     const bool fused = kCanFuse && ba.dbg != 22 && rblocks <= grid;
-    if (ba.jobs[0].ep_x && (!fused || ba.n_jobs != 1 || ba.jobs[0].NS <= 1 || !std::is_same<YT, __half>::value))
+    if (ba.ep.x && (!fused || ba.n_jobs != 1 || ba.jobs[0].NS <= 1 || !std::is_same<YT, __half>::value))
         return (int)cudaErrorInvalidConfiguration;  // the norm epilogue runs in the trailing completion CTAs
     auto kern = fused ? gemv_batch_kernel<NJ, XT, YT, ST, ASYM, kCanFuse> : gemv_batch_kernel<NJ, XT, YT, ST, ASYM, false>;
     constexpr int smem = SlotGeom<ST, ASYM>::kSmem;

@@ -66,10 +66,6 @@ static void make_job(Job& J, const abcq_model_t* m, int p, const void* x, void* 
     J.nw = nullptr;
     J.xo = nullptr;
     J.eps = 0.f;
-    J.ep_x = nullptr;
-    J.ep_w = nullptr;
-    J.ep_h = nullptr;
-    J.ep_eps = 0.f;
     J.y = y;
     J.partial = reinterpret_cast<float*>(ws);
     J.ncta = 0;
@@ -109,12 +105,6 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             a.jobs[0].xo = static_cast<__half*>(nin->x_out);
             a.jobs[0].eps = nin->eps;
         }
-        if (nout && j == 0) {
-            a.jobs[0].ep_x = static_cast<__half*>(nout->stream);
-            a.jobs[0].ep_w = static_cast<const __half*>(nout->norm_w);
-            a.jobs[0].ep_h = static_cast<__half*>(nout->h);
-            a.jobs[0].ep_eps = nout->eps;
-        }
         w += partial_bytes(models[j]);
         a.jobs[j].arrive = counters ? counters + j * kCounterStride : nullptr;
         a.jobs[j].reduced = counters ? counters + (kMaxJobs + j) * kCounterStride : nullptr;
@@ -126,6 +116,8 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
         units += (int64_t)J.items * J.w;
     }
     a.n_jobs = n;
+    a.ep = Epi{nout ? static_cast<__half*>(nout->stream) : nullptr, nout ? static_cast<const __half*>(nout->norm_w) : nullptr,
+               nout ? static_cast<__half*>(nout->h) : nullptr, nout ? nout->eps : 0.f};
     a.total_items = items;
     a.total_units = units;
     // CTA ranges: greedy fill against a common budget T, with exact piece

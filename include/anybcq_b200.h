@@ -101,15 +101,20 @@ int abcq_set_reserved_sms(int32_t n, int32_t* prev_out);
  * done, table built, stream done, reduction done) to d_buf[cta*8 + k].    */
 int abcq_debug_set_trace(void* d_buf);
 /* profiling experiments only (results are WRONG when mode is 1 or 2): 1 =
- * skip the table lookups, 2 = skip the weight loads; 23 = route single GEMVs
- * through the batch kernel instead of the cluster kernel; 32 = the batch
+ * skip the table lookups, 2 = skip the weight loads; 22 = split-K completion
+ * as the separate kernel for every batch; 23 = route single GEMVs through
+ * the batch kernel instead of the cluster kernel; 29 = the separate
+ * completion kernel's blocks in plain job order (default: jobs of more than
+ * 16 slices first); 32 = the batch
  * kernel's round-1 warp split (cost split of every round instead of slot-sized
  * chunks); 33 = batch CTAs take the schedule in reverse (placement
  * experiment); 7001 + c = per-warp round stamps of batch CTA c after the 16
  * launch slots of the trace buffer (7000 = off); 27 = route every
  * single GEMV through the cluster kernel; 5000 + 100*slots + 10*C + t = force
  * the cluster kernel's geometry (C digit 6 = 16; 5000 = automatic); 6000 + W =
- * force its consumer warps (8 / 16; 6000 = automatic). Default 0. */
+ * force its consumer warps (8 / 16; 6000 = automatic); 1000 + b / 2000 + s /
+ * 3000 + v = the batch schedule's piece cost in blocks / ring slots issued
+ * before the PDL wait / partition strategy. Default 0. */
 int abcq_debug_set_mode(int32_t mode);
 /* profiling aid: the launch geometry a single GEMV (abcq_gemv, or a batch of
  * one job) uses for this model and precision -- out7 = {cluster size C,

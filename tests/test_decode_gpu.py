@@ -291,18 +291,21 @@ def test_quantized_step_norm_out_equals_separate_add_rmsnorm():
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("rows,cols,glu", [(4096, 4096, False), (4096, 14336, True), (8192, 1024, False)])
-def test_gemv_rmsnorm_out_matches_separate_ops(rows, cols, glu):
+@pytest.mark.parametrize("rows,cols,glu,asym,sd", [(4096, 4096, False, False, "f16"), (4096, 14336, True, False, "f16"),
+                                                  (8192, 1024, False, False, "f16"), (1000, 1000, False, True, "f32"),
+                                                  (37, 300, True, True, "f16")])
+def test_gemv_rmsnorm_out_matches_separate_ops(rows, cols, glu, asym, sd):
     """The norm epilogue vs the persistent GEMV + add_rmsnorm launch (both
     bitwise): y, the updated residual stream and h; plus the usage checks."""
     import paper_2510_10467_b200 as P
     from paper_2510_10467_b200.decode import add_rmsnorm
-    dm = P.DeviceModel(rows, cols, 128, 2, 4, scale_dtype="f16")
+    dm = P.DeviceModel(rows, cols, 128, 2, 4, asym, scale_dtype=sd)
     g = torch.Generator(device="cuda").manual_seed(rows + cols)
-    dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, rows, cols // 32), dtype=torch.int32, device="cuda",
-                                 generator=g))
+    wpr, G = -(-cols // 32), -(-cols // 128)
+    dm.load_planes(torch.randint(-2**31, 2**31 - 1, (4, rows, wpr), dtype=torch.int32, device="cuda", generator=g))
     for q in (2, 3, 4):
-        dm.load_scale_set(q, (0.01 + 0.01 * torch.rand((q, rows, cols // 128), device="cuda", generator=g)) / 4)
+        z = 0.01 * torch.randn((rows, G), device="cuda", generator=g) if asym else None
+        dm.load_scale_set(q, (0.01 + 0.01 * torch.rand((q, rows, G), device="cuda", generator=g)) / 4, z)
     x = torch.randn(2 * cols if glu else cols, device="cuda", generator=g).half()
     s0 = torch.randn(rows, device="cuda", generator=g).half()
     w = (1 + 0.1 * torch.randn(rows, device="cuda", generator=g)).half()

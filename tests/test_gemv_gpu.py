@@ -472,8 +472,8 @@ def test_split_k_completion_paths_agree(P):
         assert torch.equal(o, f)
 
 
-@pytest.mark.parametrize("asym", [False, True])
-def test_batch_schedule_variants_bitwise_equal(P, asym):
+@pytest.mark.parametrize("asym,sd", [(False, "f16"), (True, "f16"), (True, "f32")])
+def test_batch_schedule_variants_bitwise_equal(P, asym, sd):
     """The schedule only decides which warp / CTA / completion block does an
     item, never the arithmetic: the slot-sized chunk split of multi-round CTAs
     vs the round-1 cost split (debug mode 32), the completion blocks of >16-slice
@@ -483,11 +483,11 @@ def test_batch_schedule_variants_bitwise_equal(P, asym):
     from paper_2510_10467_b200 import _lib
     from paper_2510_10467_b200.device_model import gemv_batch
     shapes = [(1024, 4096), (4096, 4096), (512, 14336), (2000, 1000), (16, 4096)]
-    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 1, 4, asym=asym, seed=r + c), scale_dtype="f16")
+    dms = [P.DeviceModel.from_model(synth_model(P, r, c, 1, 4, asym=asym, seed=r + c), scale_dtype=sd)
            for r, c in shapes]
     x = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for _, c in shapes}
     jobs = [(dm, p, x[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16))
-            for p in (1, 2, 3, 4) for dm in dms]
+            for p in (1, 2, 3, 4) for dm in dms]  # (f32 asymmetric scales: 4-item slots)
     gemv_batch(jobs)
     torch.cuda.synchronize()
     base = [o.clone() for *_, o in jobs]

@@ -213,6 +213,31 @@ int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n_jobs,
 int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n_jobs, void* d_workspace, size_t workspace_bytes,
                     void* stream);
 
+/* Fused all-gather (SURVEY §8e, row-sharded GEMV over `world` ranks, one
+ * process per GPU): abcq_gemv_batch whose split-K completion also stores every
+ * y row into each rank's gathered buffer over peer memory (NVLink), at the
+ * offset the row has in this rank's buffer -- the buffers are symmetric
+ * (the same layout on every rank: e.g. torch symmetric memory), and every
+ * job's y lies inside [local_base, local_base + local_bytes). When the
+ * launch's rows are all stored, its last completion block increments this
+ * rank's epoch (d_state[0]) and writes it, with release semantics at system
+ * scope, to slot [rank] of every rank's signal array (peer_signals[k]: rank
+ * k's u32[world]). peer_bases / peer_signals: HOST arrays of `world` device
+ * pointers valid on this device (peer_bases[rank] == local_base); d_state:
+ * abcq_peer_state_bytes() zero-filled once per gathered buffer, then
+ * self-maintaining. Every job must be split (cols > 256).
+ * abcq_peer_wait: a one-warp kernel that waits until every rank's slot in
+ * this rank's signal array reached this rank's epoch (the consumer's view:
+ * all ranks' rows have landed); gives up after timeout_ns, setting *d_err
+ * to 1 + the first late rank, rather than hang.                            */
+size_t abcq_peer_state_bytes(void);
+int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n_jobs, const void* d_local_base, size_t local_bytes,
+                         void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                         uint32_t* d_state, void* d_workspace, size_t workspace_bytes, void* stream);
+int abcq_peer_wait(const uint32_t* d_signals, int32_t world, const uint32_t* d_state, uint32_t* d_err,
+                   int64_t timeout_ns, void* stream);
+
+
 /* ---- small-batch GEMM with per-request precision --------------------------
  * Replaces the reference's per-request loop (cli.py:122-126 loops
  * GemvEngine.lut over the rows of x; service/server.py:188-206 serves one

@@ -281,7 +281,8 @@ int abcq_gemv_batch_workspace_bytes(const abcq_gemv_job_t* jobs, int32_t n, size
     return 0;
 }
 
-int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t ws_bytes, void* stream) {
+static int batch_launch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t ws_bytes, void* stream,
+                        const abcq::PeerOut* pout, const char* what) {
     size_t need = 0;
     if (int rc = abcq_gemv_batch_workspace_bytes(jobs, n, &need)) return rc;
     if (need && (!d_ws || ws_bytes < need))
@@ -298,10 +299,56 @@ int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t w
         xs[j] = jobs[j].x;
         ys[j] = jobs[j].y;
     }
-    return cuda_ret(abcq::launch_gemv_jobs(models, ps, xs, ys, n, xds, jobs[0].y_dtype, d_ws,
-                                           (cudaStream_t)stream),
-                    "abcq_gemv_batch");
+    return cuda_ret(abcq::launch_gemv_jobs(models, ps, xs, ys, n, xds, jobs[0].y_dtype, d_ws, (cudaStream_t)stream,
+                                           nullptr, nullptr, pout),
+                    what);
 }
+
+size_t abcq_peer_state_bytes(void) { return 256; }
+
+int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n, const void* d_local_base, size_t local_bytes,
+                         void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                         uint32_t* d_state, void* d_ws, size_t ws_bytes, void* stream) {
+    if (world < 1 || world > abcq::kMaxPeerRanks || rank < 0 || rank >= world)
+        return fail(ABCQ_E_ARG, "world %d / rank %d outside 1..%d", world, rank, abcq::kMaxPeerRanks);
+    if (!d_local_base || !peer_bases || !peer_signals || !d_state)
+        return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: NULL buffer");
+    if (peer_bases[rank] != d_local_base)
+        return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: peer_bases[rank] must be the local buffer");
+    abcq::PeerOut po{};
+    po.n = world;
+    po.rank = rank;
+    po.local_base = d_local_base;
+    po.state = d_state;
+    const char* lo = static_cast<const char*>(d_local_base);
+    for (int k = 0; k < world; ++k) {
+        if (!peer_bases[k] || !peer_signals[k]) return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: rank %d NULL", k);
+        po.base[k] = peer_bases[k];
+        po.sig[k] = peer_signals[k];
+    }
+    for (int j = 0; j < n && jobs; ++j) {  // every output inside the symmetric buffer, f16/f32 rows, split
+        const char* y = static_cast<const char*>(jobs[j].y);
+        const size_t ysz = (size_t)(jobs[j].model ? jobs[j].model->rows : 0) * (jobs[j].y_dtype == ABCQ_F32 ? 4 : 2);
+        if (y < lo || y + ysz > lo + local_bytes)
+            return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: job %d's y is outside the gathered buffer", j);
+        if (jobs[j].model && jobs[j].model->cols <= 256)
+            return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: job %d has one slice (cols <= 256): no completion pass", j);
+    }
+    return batch_launch(jobs, n, d_ws, ws_bytes, stream, &po, "abcq_gemv_batch_peer");
+}
+
+int abcq_peer_wait(const uint32_t* d_signals, int32_t world, const uint32_t* d_state, uint32_t* d_err,
+                   int64_t timeout_ns, void* stream) {
+    if (world < 1 || world > abcq::kMaxPeerRanks || !d_signals || !d_state || !d_err)
+        return fail(ABCQ_E_ARG, "abcq_peer_wait: bad arguments");
+    return cuda_ret(abcq::launch_peer_wait(d_signals, world, d_state, d_err, timeout_ns, (cudaStream_t)stream),
+                    "abcq_peer_wait");
+}
+
+int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t ws_bytes, void* stream) {
+    return batch_launch(jobs, n, d_ws, ws_bytes, stream, nullptr, "abcq_gemv_batch");
+}
+
 
 int abcq_gemm_mixedp_max_batch(void) { return 16; }
 

@@ -58,6 +58,22 @@ struct Epi {
     float eps;
 };
 
+// fused all-gather (abcq_gemv_batch_peer): every completed y row is also
+// stored into each peer rank's gathered buffer at the same offset
+// (symmetric layout, peer memory over NVLink), and the launch's last
+// completion block bumps this rank's epoch and publishes it in slot [rank]
+// of every peer's signal array (release, system scope)
+constexpr int kMaxPeers = 8;
+struct Peers {
+    int n;                     // ranks (0: no peer outputs)
+    int rank;                  // this rank (its own buffer is local_base: not stored twice)
+    const char* local_base;    // this rank's gathered buffer
+    char* base[kMaxPeers];     // rank q's gathered buffer
+    uint32_t* sig[kMaxPeers];  // rank q's signal slots [n]
+    uint32_t* state;           // this rank's [0] epoch, [32] completion blocks done (self-resetting)
+    int total_blocks;          // completion blocks of the launch
+};
+
 // kernel parameter: NJ job slots (1, 8 or 32 -- the smallest that fits)
 constexpr int kMaxGrid = 192;  // CTAs (one per SM)
 
@@ -77,6 +93,7 @@ struct KArgs {
     unsigned long long* rtrace;  // per-warp round stamps of CTA rtrace_cta (profiling), or NULL
     int rtrace_cta;
     Epi ep;                      // norm epilogue of job 0 (abcq_gemv_rmsnorm_out), ep.x == NULL: none
+    Peers pe;                    // fused all-gather (abcq_gemv_batch_peer), pe.n == 0: none
 };
 
 struct BatchArgs {
@@ -94,6 +111,7 @@ struct BatchArgs {
     unsigned long long* rtrace;
     int rtrace_cta;
     Epi ep;
+    Peers pe;
 };
 
 template <typename ST, bool ASYM>
@@ -349,7 +367,16 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
         for (int u = 1; u < CPT; ++u) tot += c[q][u];  // CPT == 2: c0+c1 | c2+c3
 #pragma unroll
         for (int w = 1; w < kReduceTPR; w <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);  // (c0+c1)+(c2+c3)
-        if (sub == 0 && row[q] < J.rows) static_cast<YT*>(J.y)[row[q]] = from_f32<YT>(tot);
+        if (sub == 0 && row[q] < J.rows) {
+            YT* yr = static_cast<YT*>(J.y) + row[q];
+            const YT v = from_f32<YT>(tot);
+            *yr = v;
+            if (a.pe.n) {  // the same row into every peer's gathered buffer (NVLink stores)
+                const int64_t off = reinterpret_cast<const char*>(yr) - a.pe.local_base;
+                for (int k = 0; k < a.pe.n; ++k)
+                    if (k != a.pe.rank) *reinterpret_cast<YT*>(a.pe.base[k] + off) = v;
+            }
+        }
     }
     const bool epi = j == 0 && a.ep.x != nullptr;
     if (epi) __threadfence();  // release the y rows to the block that runs the norm epilogue
@@ -368,6 +395,17 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
         if (last) {  // last block of job j: recycle
             *J.arrive = 0u;
             *J.reduced = 0u;
+        }
+        if (a.pe.n) {  // fused all-gather: the launch's last completion block signals every rank
+            __threadfence_system();  // this block's peer stores (ordered by the barrier above) reach the peers
+            if (atomicAdd(a.pe.state + 32, 1u) == (uint32_t)(a.pe.total_blocks - 1)) {
+                __threadfence_system();
+                const uint32_t e = a.pe.state[0] + 1u;
+                a.pe.state[0] = e;
+                a.pe.state[32] = 0u;
+                for (int k = 0; k < a.pe.n; ++k)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.pe.sig[k] + a.pe.rank), "r"(e) : "memory");
+            }
         }
     }
     if (epi) return __syncthreads_or(last) ? j : -1;  // (block-uniform)
@@ -872,6 +910,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     a.rtrace = ba.rtrace;
     a.rtrace_cta = ba.rtrace_cta;
     a.ep = ba.ep;
+    a.pe = ba.pe;
     int rblocks = 0;  // split-K completion blocks (rows / (kBThreads/4) per job)
     constexpr int kFusedRows = kBThreads / kReduceTPR;
     for (int j = 0; j < ba.n_jobs; ++j)
@@ -901,6 +940,14 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
         }
         attr_set[dev] = true;
     }
+    int sep_blocks = 0;  // blocks of the separate completion kernel
+    for (int j = 0; j < ba.n_jobs; ++j)
+        if (ba.jobs[j].NS > 1) sep_blocks += (ba.jobs[j].rows + kReduceRows - 1) / kReduceRows;
+    if (a.pe.n) {
+        for (int j = 0; j < ba.n_jobs; ++j)
+            if (ba.jobs[j].NS <= 1) return (int)cudaErrorInvalidConfiguration;  // peer rows leave through the completion
+        a.pe.total_blocks = fused ? rblocks : sep_blocks;
+    }
     cudaLaunchConfig_t cfg = {};
     const bool separate = !fused;
     cfg.gridDim = dim3(grid + (separate ? 0 : rblocks));
@@ -914,9 +961,7 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e != cudaSuccess || !separate) return (int)e;
-    int nblocks = 0;  // one separate reduce launch
-    for (int j = 0; j < a.n_jobs; ++j)
-        if (a.jobs[j].NS > 1) nblocks += (a.jobs[j].rows + kReduceRows - 1) / kReduceRows;
+    const int nblocks = sep_blocks;  // one separate reduce launch
     if (nblocks == 0) return 0;
     cudaLaunchConfig_t rc = cfg;
     rc.blockDim = dim3(kReduceThreads);

@@ -79,7 +79,7 @@ static int launch_yt(const BatchArgs& a, int yd, int sd, bool asym, int grid, cu
 
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
                      int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin,
-                     const NormOut* nout) {
+                     const NormOut* nout, const PeerOut* pout) {
     BatchArgs a;  // passed by value (kernel parameter space)
     // one CTA per SM, minus the SMs reserved for kernels that run beside the
     // GEMV (e.g. an NCCL collective on another stream overlapping it)
@@ -116,6 +116,18 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
         units += (int64_t)J.items * J.w;
     }
     a.n_jobs = n;
+    a.pe = Peers{};
+    if (pout) {
+        static_assert(kMaxPeers == kMaxPeerRanks, "peer slots");
+        a.pe.n = pout->n;
+        a.pe.rank = pout->rank;
+        a.pe.local_base = static_cast<const char*>(pout->local_base);
+        for (int k = 0; k < pout->n; ++k) {
+            a.pe.base[k] = static_cast<char*>(pout->base[k]);
+            a.pe.sig[k] = pout->sig[k];
+        }
+        a.pe.state = pout->state;
+    }
     a.ep = Epi{nout ? static_cast<__half*>(nout->stream) : nullptr, nout ? static_cast<const __half*>(nout->norm_w) : nullptr,
                nout ? static_cast<__half*>(nout->h) : nullptr, nout ? nout->eps : 0.f};
     a.total_items = items;
@@ -242,6 +254,35 @@ int launch_gemv_add_rmsnorm(const abcq_model_t* m, int p, const NormIn& nin, voi
 int launch_gemv_rmsnorm_out(const abcq_model_t* m, int p, const void* x, int x_dtype, void* y, const NormOut& nout,
                             void* ws, cudaStream_t st) {
     return launch_gemv_jobs(&m, &p, &x, &y, 1, &x_dtype, ABCQ_F16, ws, st, nullptr, &nout);
+}
+
+// consumer side of the fused all-gather: wait (one warp, lane k polls rank k's
+// slot with acquire loads at system scope) until every rank published this
+// rank's current epoch; gives up after timeout_ns and sets *err = 1 + k
+// instead of hanging
+__global__ void peer_wait_kernel(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err,
+                                 long long timeout_ns) {
+    pdl_wait();
+    const int k = threadIdx.x;
+    if (k >= n) return;
+    const uint32_t want = *reinterpret_cast<const volatile uint32_t*>(state);
+    const unsigned long long t0 = globaltimer();
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sig + k) : "memory");
+        if ((int32_t)(v - want) >= 0) break;
+        if ((long long)(globaltimer() - t0) > timeout_ns) {
+            atomicCAS(err, 0u, 1u + (uint32_t)k);
+            break;
+        }
+        __nanosleep(64);
+    }
+}
+
+int launch_peer_wait(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err, long long timeout_ns,
+                     cudaStream_t st) {
+    peer_wait_kernel<<<1, 32, 0, st>>>(sig, n, state, err, timeout_ns);
+    return (int)cudaGetLastError();
 }
 
 }  // namespace abcq

@@ -27,9 +27,21 @@ int launch_gemv_lut(const abcq_model_t* m, int p, const void* x, int x_dtype, vo
 // in job order (lut_workspace_bytes each)
 struct NormIn;
 struct NormOut;
+struct PeerOut;
 int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const void* const* xs, void* const* ys,
                      int n, const int* x_dtypes, int y_dtype, void* ws, cudaStream_t st, const NormIn* nin = nullptr,
-                     const NormOut* nout = nullptr);
+                     const NormOut* nout = nullptr, const PeerOut* pout = nullptr);
+// fused all-gather (abcq_gemv_batch_peer): see Peers in abcq_gemv_batch.cuh
+constexpr int kMaxPeerRanks = 8;
+struct PeerOut {
+    int n, rank;
+    const void* local_base;
+    void* base[kMaxPeerRanks];
+    uint32_t* sig[kMaxPeerRanks];
+    uint32_t* state;
+};
+int launch_peer_wait(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err, long long timeout_ns,
+                     cudaStream_t st);
 int lut_max_jobs();
 
 // fused input mode of the persistent GEMV: input = f16(f16(x + residual) * inv_rms * norm_w),

@@ -137,3 +137,82 @@ class RowShardedGemv:
         self.local(p, x)
         self.gather()
         return self.y
+
+
+class PeerGather:
+    """The fused all-gather's buffer: a gathered output
+    of `world * rows_per_rank` elements in torch symmetric memory -- every
+    rank's copy and signal pad mapped on every GPU (NVLink peer memory) -- so
+    that a GEMV launch stores its rows straight into all ranks' copies
+    (abcq_gemv_batch_peer) instead of a separate NCCL all-gather. Rank r's
+    rows are `local` = buffer[r*R:(r+1)*R]; `plan(jobs)` builds the launch
+    (jobs' outputs must be views of `local`); `wait()` enqueues the consumer
+    wait (every rank's rows of the latest launch have landed)."""
+
+    def __init__(self, rows_per_rank: int, group=None, dtype=torch.float16, device=None):
+        import ctypes as C
+
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _lib
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if self.world > 8:
+            raise UsageError("the fused all-gather supports up to 8 ranks (one NVLink domain node)")
+        self.rows = int(rows_per_rank)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buffer = symm_mem.empty(self.world * self.rows, dtype=dtype, device=dev)
+        self.handle = symm_mem.rendezvous(self.buffer, self.group.group_name)
+        self.local = self.buffer[self.rank * self.rows:(self.rank + 1) * self.rows]
+        self._bases = (C.c_void_p * self.world)(*[int(v) for v in self.handle.buffer_ptrs])
+        self._sigs = (C.c_void_p * self.world)(*[int(v) for v in self.handle.signal_pad_ptrs])
+        if int(self._bases[self.rank]) != self.buffer.data_ptr():
+            raise UsageError("symmetric memory: this rank's buffer pointer mismatch")
+        n = int(_lib.lib().abcq_peer_state_bytes())
+        self.state = torch.zeros(n // 4, dtype=torch.int32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._C, self._lib = C, _lib
+
+    def plan(self, jobs) -> "PeerGemvPlan":
+        return PeerGemvPlan(self, jobs)
+
+    def wait(self, stream=None, timeout_s: float = 2.0) -> None:
+        """Enqueue: block the stream until every rank's rows of the latest
+        launch are in this rank's buffer (bounded: `err` = 1 + the late rank)."""
+        from .device_model import _stream_handle
+        sig = int(self._sigs[self.rank])
+        self._lib.check(self._lib.lib().abcq_peer_wait(sig, self.world, self.state.data_ptr(), self.err.data_ptr(),
+                                                       int(timeout_s * 1e9), _stream_handle(stream)),
+                        "abcq_peer_wait")
+
+
+class PeerGemvPlan:
+    """A GemvBatchPlan whose launch also stores every output row into all
+    ranks' PeerGather buffers (one launch: GEMV + all-gather)."""
+
+    def __init__(self, gather: PeerGather, jobs):
+        from .device_model import GemvBatchPlan
+        lo = gather.local.data_ptr()
+        hi = lo + gather.local.numel() * gather.local.element_size()
+        for _, _, _, out in jobs:
+            if not lo <= out.data_ptr() < hi:
+                raise UsageError("PeerGemvPlan: every output must be a view of the gather's `local` rows")
+        self.gather = gather
+        self.base = GemvBatchPlan(jobs)
+
+    def launch(self, stream=None):
+        from .device_model import _stream_handle
+        b, g = self.base, self.gather
+        for dm, p, _, _ in b.jobs:
+            if dm._level_ready:
+                dm._order_after_upload(p, stream)
+        sh = _stream_handle(stream)
+        ws = b._ws.get(sh)
+        if ws is None:
+            ws = b._ws[sh] = torch.zeros(b.need, dtype=torch.uint8, device=b.device)
+        nbytes = g.buffer.numel() * g.buffer.element_size()
+        g._lib.check(b._L.abcq_gemv_batch_peer(b.arr, b.n, g.buffer.data_ptr(), nbytes, g._bases, g._sigs, g.world,
+                                               g.rank, g.state.data_ptr(), ws.data_ptr(), ws.numel(), sh),
+                     "abcq_gemv_batch_peer")
+        return [j[3] for j in b.jobs]

@@ -758,3 +758,89 @@ def test_row_sharded_gemv_nccl_world1(P):
         torch.cuda.synchronize()
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_peer_allgather_world1(P):
+    """The fused all-gather (abcq_gemv_batch_peer through torch symmetric
+    memory) at world size 1: the rows land in the gathered buffer bitwise as
+    a plain batch launch writes them, the epoch advances once per launch and
+    is published in the signal slot, the consumer wait passes (no timeout),
+    and the host checks reject outputs outside the buffer / one-slice jobs."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2510_10467_b200.device_model import gemv_batch
+    from paper_2510_10467_b200.parallel import PeerGather
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shapes = [(4096, 4096), (1000, 2048), (512, 14336)]
+        dms = [P.DeviceModel.from_model(synth_model(P, r, c, 2, 4, seed=r + c), scale_dtype="f16") for r, c in shapes]
+        x = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for _, c in shapes}
+        specs = [(dm, p) for p in (2, 4) for dm in dms]
+        R = sum(dm.rows for dm, _ in specs)
+        g = PeerGather(R)
+        views, off = [], 0
+        for dm, _ in specs:
+            views.append(g.local[off:off + dm.rows])
+            off += dm.rows
+        plan = g.plan([(dm, p, x[dm.cols], v) for (dm, p), v in zip(specs, views)])
+        want = gemv_batch([(dm, p, x[dm.cols], torch.empty(dm.rows, device="cuda", dtype=torch.float16))
+                           for dm, p in specs])
+        for it in (1, 2, 3):
+            g.local.fill_(0)
+            plan.launch()
+            g.wait()
+            torch.cuda.synchronize()
+            assert int(g.err.item()) == 0
+            assert int(g.state[0].item()) == it
+            for v, w in zip(views, want):
+                assert torch.equal(v, w)
+        with pytest.raises(P.UsageError):  # an output outside the gathered rows
+            g.plan([(dms[0], 2, x[4096], torch.empty(4096, device="cuda", dtype=torch.float16))])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_stores_two_buffers_one_gpu(P):
+    """The peer-store data path on one GPU: a 2-'rank' launch whose 'peer'
+    buffer is a second local buffer -- rank 0's rows land in both buffers at
+    the same offsets (bitwise), the epoch is published in both signal arrays,
+    and the C-ABI argument checks hold (peer_bases[rank] must be local)."""
+    import ctypes as C
+
+    from paper_2510_10467_b200 import _lib
+    from paper_2510_10467_b200.device_model import GemvBatchPlan, gemv_batch
+    L = _lib.lib()
+    dms = [P.DeviceModel.from_model(synth_model(P, r, 4096, 2, 4, seed=r), scale_dtype="f16") for r in (4096, 1024)]
+    x = torch.from_numpy(O.random_gaussian(1, 4096, seed=3).ravel()).cuda().half()
+    R = sum(dm.rows for dm in dms)
+    buf = [torch.zeros(2 * R, dtype=torch.float16, device="cuda") for _ in range(2)]  # 2 'ranks' x R rows
+    sig = [torch.zeros(8, dtype=torch.int32, device="cuda") for _ in range(2)]
+    state = torch.zeros(int(L.abcq_peer_state_bytes()) // 4, dtype=torch.int32, device="cuda")
+    views, off = [], 0
+    for dm in dms:
+        views.append(buf[0][off:off + dm.rows])  # rank 0's slice of its own buffer
+        off += dm.rows
+    plan = GemvBatchPlan([(dm, 3, x, v) for dm, v in zip(dms, views)])
+    ws = torch.zeros(plan.need, dtype=torch.uint8, device="cuda")
+    bases = (C.c_void_p * 2)(buf[0].data_ptr(), buf[1].data_ptr())
+    sigs = (C.c_void_p * 2)(sig[0].data_ptr(), sig[1].data_ptr())
+    sh = torch.cuda.current_stream().cuda_stream
+    for it in (1, 2):
+        _lib.check(L.abcq_gemv_batch_peer(plan.arr, plan.n, buf[0].data_ptr(), buf[0].numel() * 2, bases, sigs, 2, 0,
+                                          state.data_ptr(), ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch_peer")
+        torch.cuda.synchronize()
+        want = gemv_batch([(dm, 3, x, torch.empty(dm.rows, device="cuda", dtype=torch.float16)) for dm in dms])
+        assert torch.equal(buf[0][:R], torch.cat(want)) and torch.equal(buf[1][:R], buf[0][:R])
+        assert int(state[0]) == it and int(sig[0][0]) == it and int(sig[1][0]) == it
+    assert not buf[1][R:].any()  # rank 1's rows: nobody wrote them
+    swapped = (C.c_void_p * 2)(buf[1].data_ptr(), buf[0].data_ptr())
+    with pytest.raises(P.UsageError):
+        _lib.check(L.abcq_gemv_batch_peer(plan.arr, plan.n, buf[0].data_ptr(), buf[0].numel() * 2, swapped, sigs, 2, 0,
+                                          state.data_ptr(), ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch_peer")

@@ -346,6 +346,28 @@ def run_gpu(args):
     mp_work = [None, None]
     mp_plan = [P.GemvBatchPlan([(models[pi][li], p, xs[models[pi][li].cols], mp_views[b][n])
                                 for n, (pi, p, li) in enumerate(all_jobs)]) for b in range(2)] if mp else None
+    # the product's multi-GPU step: the all-gather FUSED into the GEMV launch --
+    # its split-K completion stores every row into all ranks' symmetric buffers
+    # over NVLink peer memory (abcq_gemv_batch_peer); NCCL (above) if torch
+    # symmetric memory is unavailable or ABCQ_BENCH_ALLGATHER=nccl
+    ag_mode, peer, peer_plan = "nccl", None, None
+    if mp and os.environ.get("ABCQ_BENCH_ALLGATHER", "peer") == "peer":
+        try:
+            from paper_2510_10467_b200.parallel import PeerGather
+            peer = PeerGather(mp_rows, device=dev)
+            off, pv = 0, []
+            for pi, p, li in all_jobs:
+                pv.append(peer.local[off:off + models[pi][li].rows])
+                off += models[pi][li].rows
+            peer_plan = peer.plan([(models[pi][li], p, xs[models[pi][li].cols], pv[n])
+                                   for n, (pi, p, li) in enumerate(all_jobs)])
+            ag_mode = "peer"
+        except Exception as exc:  # noqa: BLE001
+            peer = peer_plan = None
+            ag_mode = f"nccl (fused peer all-gather unavailable: {str(exc)[:100]})"
+    if mp_reserve and ag_mode == "peer":  # no collective kernel beside the GEMV grid
+        P.set_reserved_sms(0)
+        mp_reserve = 0
 
     def step_mp(i):
         b = i & 1
@@ -400,6 +422,10 @@ def run_gpu(args):
             for _ in range(n):
                 step_launches()
             return
+        if peer_plan is not None:
+            for _ in range(n):
+                peer_plan.launch(stream)
+            return
         side.wait_stream(stream)
         for i in range(n):
             step_mp_graphed(i)
@@ -444,6 +470,9 @@ def run_gpu(args):
             if use_graph:
                 for g, _ in plan:
                     g.replay()
+            elif peer_plan is not None:
+                for i in range(args.steps):
+                    peer_plan.launch(stream)
             else:
                 for i in range(args.steps):
                     step_mp(i)
@@ -459,6 +488,47 @@ def run_gpu(args):
         dist.barrier()
     ms_step = ms / args.steps
     value = step_bytes() * world / (ms_step * 1e-3) / 1e9
+    ag_check = None
+    if peer is not None:  # every rank's latest rows in this rank's buffer == an NCCL all-gather of them
+        with torch.cuda.stream(stream):
+            peer.wait(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ref = torch.empty_like(peer.buffer)
+        dist.all_gather_into_tensor(ref, peer.local.clone())
+        torch.cuda.synchronize()
+        ag_check = bool(torch.equal(ref, peer.buffer)) and int(peer.err.item()) == 0
+    ag_alt = None
+    if peer is not None:  # the baseline beside it: the same GEMV steps + an NCCL all-gather on a side stream
+        try:
+            rsv = MP_RESERVE_SMS if world > 1 else 0
+            P.set_reserved_sms(rsv)  # (the collective's SMs, as in the NCCL mode)
+            n_alt = min(args.steps, 50)
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2, stream=stream):
+                side.wait_stream(stream)
+                for i in range(n_alt):
+                    step_mp_graphed(i)
+                stream.wait_stream(side)
+            with torch.cuda.stream(stream):
+                g2.replay()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a2.record(stream)
+                g2.replay()
+                b2.record(stream)
+            torch.cuda.synchronize()
+            t2 = torch.tensor([a2.elapsed_time(b2)], device=dev)
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+            ms2 = float(t2.item()) / n_alt
+            ag_alt = {"allgather": f"nccl on a side stream overlapping the next GEMV ({rsv} SMs reserved)",
+                      "ms_per_step": round(ms2, 5), "value": round(step_bytes() * world / (ms2 * 1e-3) / 1e9, 1)}
+            P.set_reserved_sms(0)
+            del g2
+        except Exception as exc:  # noqa: BLE001
+            ag_alt = {"error": str(exc)[:120]}
 
     peak, peak_kind = read_peaks()
     sections = set(args.sections.split(",")) if args.sections else None
@@ -509,6 +579,10 @@ def run_gpu(args):
                                   "per step overlapping the next step (double-buffered), CUDA events, max over ranks"))
         if mp_reserve:
             timing += f"; the GEMV grid leaves {mp_reserve} SMs to the all-gather (NCCL_MAX_CTAS={mp_reserve})"
+        if peer is not None:
+            timing = ("the K steps captured as CUDA graphs of <= 50 steps, each step ONE GEMV launch whose split-K "
+                      "completion also stores its rows into every rank's symmetric buffer over NVLink peer memory "
+                      "(the all-gather fused into the GEMV, abcq_gemv_batch_peer), CUDA events, max over ranks")
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -529,6 +603,10 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "config5": cfg5,
         }
+        if mp:
+            line["allgather"] = ag_mode
+            line["allgather_check"] = ag_check
+            line["allgather_nccl_variant"] = ag_alt
         line.update(out)
         print(json.dumps(line))
     if mp:
@@ -969,6 +1047,21 @@ def config5_row_sharded(ctx, args, peak):
         if e is not None:
             e.x_buffer.copy_(xs[e.cols])
     res = {"n_gpus": world}
+    # fused all-gather buffers (one symmetric buffer per layer, rank r's rows
+    # at r * per-rank rows) when a process group exists
+    peers, peer_plans = [], {}
+    if dist.is_initialized() and all(e is not None for e in engines):
+        try:
+            from paper_2510_10467_b200.parallel import PeerGather
+            for li, (name, r, k) in enumerate(LAYERS_70B):
+                lo0, hi0 = row_shard_bounds(r, world, 0)
+                peers.append(PeerGather(hi0 - lo0, device=ctx.dev))
+            for p in (2, 4):
+                peer_plans[p] = [pg.plan([(e.dm, p, e.x_buffer, pg.local[:e.dm.rows])])
+                                 for e, pg in zip(engines, peers)]
+        except Exception as exc:  # noqa: BLE001
+            peers, peer_plans = [], {}
+            res["fused_allgather"] = f"unavailable: {str(exc)[:100]}"
     for p in (2, 4):
         def local_all():
             for e in engines:
@@ -1008,18 +1101,36 @@ def config5_row_sharded(ctx, args, peak):
             torch.cuda.synchronize()
             full_ms = a.elapsed_time(b) / n
             mode = "eager"
-        t = torch.tensor([gemv_ms, full_ms], device=ctx.dev)
+        # the product path: each layer's all-gather FUSED into its GEMV launch
+        # (rows stored into every rank's symmetric buffer, abcq_gemv_batch_peer),
+        # then the consumer wait (every rank's rows landed) before the next layer
+        peer_ms = None
+        if peers:
+            if world > 1:
+                dist.barrier()
+
+            def peer_all():
+                for pp_, pg in zip(peer_plans[p], peers):
+                    pp_.launch(ctx.stream)
+                    pg.wait(ctx.stream)
+
+            peer_ms = ctx.time_graph(peer_all, reps=10)
+        t = torch.tensor([gemv_ms, full_ms, peer_ms or 0.0], device=ctx.dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gemv_ms, full_ms = (float(v) for v in t.tolist())
+        gemv_ms, full_ms, peer_ms2 = (float(v) for v in t.tolist())
         total = sum(algo_bytes(r, k, p) for _, r, k in LAYERS_70B)
         res[f"p{p}"] = {"gemv_us_per_layer_set": round(gemv_ms * 1e3, 2),
                         "gemv_allgather_us_per_layer_set": round(full_ms * 1e3, 2), "allgather_timing": mode,
+                        "gemv_fused_allgather_us_per_layer_set": round(peer_ms2 * 1e3, 2) if peers else None,
                         "GBps_total": round(total / (gemv_ms * 1e-3) / 1e9, 1),
                         "roofline_frac_per_gpu": round(total / world / (gemv_ms * 1e-3) / 1e9 / peak, 4)}
     del engines
+    del peers, peer_plans
     res["what"] = ("Llama-3-70B layer set (q,k,v,o,gate,up,down) row-sharded over n_gpus; GBps_total = the "
-                   "whole layer set's algorithmic bytes / GEMV time; all-gather of each layer's fp16 output")
+                   "whole layer set's algorithmic bytes / GEMV time; all-gather of each layer's fp16 output: NCCL "
+                   "after the GEMV (gemv_allgather_*) or fused into it -- rows stored into every rank's symmetric "
+                   "buffer by the GEMV's completion, then the consumer wait (gemv_fused_allgather_*)")
     return res
 
 

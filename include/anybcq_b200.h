@@ -218,24 +218,26 @@ int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n_jobs, void* d_workspa
  * y row into each rank's gathered buffer over peer memory (NVLink), at the
  * offset the row has in this rank's buffer -- the buffers are symmetric
  * (the same layout on every rank: e.g. torch symmetric memory), and every
- * job's y lies inside [local_base, local_base + local_bytes). When the
- * launch's rows are all stored, its last completion block increments this
- * rank's epoch (d_state[0]) and writes it, with release semantics at system
- * scope, to slot [rank] of every rank's signal array (peer_signals[k]: rank
- * k's u32[world]). peer_bases / peer_signals: HOST arrays of `world` device
- * pointers valid on this device (peer_bases[rank] == local_base); d_state:
- * abcq_peer_state_bytes() zero-filled once per gathered buffer, then
- * self-maintaining. Every job must be split (cols > 256).
- * abcq_peer_wait: a one-warp kernel that waits until every rank's slot in
- * this rank's signal array reached this rank's epoch (the consumer's view:
- * all ranks' rows have landed); gives up after timeout_ns, setting *d_err
- * to 1 + the first late rank, rather than hang.                            */
+ * job's y lies inside [local_base, local_base + local_bytes). Publication is
+ * deferred by one launch: the next abcq_gemv_batch_peer (or abcq_peer_wait)
+ * on this rank, once past its PDL wait, fences at system scope, increments
+ * this rank's epoch (d_state[0]) and writes it to slot [rank] of every rank's
+ * signal array -- from the GEMV grid's last CTA, so the fence is off the
+ * critical path. peer_bases / peer_signals: HOST arrays of `world` device
+ * pointers valid on this device (peer_bases[rank] == local_base; rank k's
+ * signals: u32[world]); d_state: abcq_peer_state_bytes() zero-filled once per
+ * gathered buffer. Every job must be split (cols > 256).
+ * abcq_peer_wait: a one-warp kernel that publishes this rank's pending launch
+ * and waits until every rank's slot in this rank's signal array reached this
+ * rank's epoch (all ranks' rows of the latest launch have landed); gives up
+ * after timeout_ns, setting *d_err to 1 + the first late rank, rather than
+ * hang. Every rank calls it after the same launch (SPMD).                   */
 size_t abcq_peer_state_bytes(void);
 int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n_jobs, const void* d_local_base, size_t local_bytes,
                          void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
                          uint32_t* d_state, void* d_workspace, size_t workspace_bytes, void* stream);
-int abcq_peer_wait(const uint32_t* d_signals, int32_t world, const uint32_t* d_state, uint32_t* d_err,
-                   int64_t timeout_ns, void* stream);
+int abcq_peer_wait(void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                   uint32_t* d_state, uint32_t* d_err, int64_t timeout_ns, void* stream);
 
 
 /* ---- small-batch GEMM with per-request precision --------------------------

@@ -90,7 +90,7 @@ SIGNATURES = {
     "abcq_peer_state_bytes": (C.c_size_t, []),
     "abcq_gemv_batch_peer": (C.c_int, [_PJ, _i32, _vp, _sz, C.POINTER(_vp), C.POINTER(_vp), _i32, _i32, _vp, _vp, _sz,
                                        _vp]),
-    "abcq_peer_wait": (C.c_int, [_vp, _i32, _vp, _vp, _i64, _vp]),
+    "abcq_peer_wait": (C.c_int, [C.POINTER(_vp), C.POINTER(_vp), _i32, _i32, _vp, _vp, _i64, _vp]),
     "abcq_gemv_batch_max_jobs": (C.c_int, []),
     "abcq_gemv_batch_workspace_bytes": (C.c_int, [_PJ, _i32, C.POINTER(_sz)]),
     "abcq_gemv_batch": (C.c_int, [_PJ, _i32, _vp, _sz, _vp]),

@@ -306,27 +306,33 @@ static int batch_launch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size
 
 size_t abcq_peer_state_bytes(void) { return 256; }
 
-int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n, const void* d_local_base, size_t local_bytes,
-                         void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
-                         uint32_t* d_state, void* d_ws, size_t ws_bytes, void* stream) {
+static int peer_out(void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                    const void* d_local_base, uint32_t* d_state, abcq::PeerOut& po) {
     if (world < 1 || world > abcq::kMaxPeerRanks || rank < 0 || rank >= world)
         return fail(ABCQ_E_ARG, "world %d / rank %d outside 1..%d", world, rank, abcq::kMaxPeerRanks);
-    if (!d_local_base || !peer_bases || !peer_signals || !d_state)
-        return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: NULL buffer");
+    if (!d_local_base || !peer_bases || !peer_signals || !d_state) return fail(ABCQ_E_ARG, "fused all-gather: NULL buffer");
     if (peer_bases[rank] != d_local_base)
-        return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: peer_bases[rank] must be the local buffer");
-    abcq::PeerOut po{};
+        return fail(ABCQ_E_ARG, "fused all-gather: peer_bases[rank] must be the local buffer");
+    po = abcq::PeerOut{};
     po.n = world;
     po.rank = rank;
     po.local_base = d_local_base;
     po.state = d_state;
-    const char* lo = static_cast<const char*>(d_local_base);
     for (int k = 0; k < world; ++k) {
-        if (!peer_bases[k] || !peer_signals[k]) return fail(ABCQ_E_ARG, "abcq_gemv_batch_peer: rank %d NULL", k);
+        if (!peer_bases[k] || !peer_signals[k]) return fail(ABCQ_E_ARG, "fused all-gather: rank %d NULL", k);
         po.base[k] = peer_bases[k];
         po.sig[k] = peer_signals[k];
     }
-    for (int j = 0; j < n && jobs; ++j) {  // every output inside the symmetric buffer, f16/f32 rows, split
+    return 0;
+}
+
+int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n, const void* d_local_base, size_t local_bytes,
+                         void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                         uint32_t* d_state, void* d_ws, size_t ws_bytes, void* stream) {
+    abcq::PeerOut po;
+    if (int rc = peer_out(peer_bases, peer_signals, world, rank, d_local_base, d_state, po)) return rc;
+    const char* lo = static_cast<const char*>(d_local_base);
+    for (int j = 0; j < n && jobs; ++j) {  // every output inside the symmetric buffer, split jobs
         const char* y = static_cast<const char*>(jobs[j].y);
         const size_t ysz = (size_t)(jobs[j].model ? jobs[j].model->rows : 0) * (jobs[j].y_dtype == ABCQ_F32 ? 4 : 2);
         if (y < lo || y + ysz > lo + local_bytes)
@@ -337,12 +343,14 @@ int abcq_gemv_batch_peer(const abcq_gemv_job_t* jobs, int32_t n, const void* d_l
     return batch_launch(jobs, n, d_ws, ws_bytes, stream, &po, "abcq_gemv_batch_peer");
 }
 
-int abcq_peer_wait(const uint32_t* d_signals, int32_t world, const uint32_t* d_state, uint32_t* d_err,
-                   int64_t timeout_ns, void* stream) {
-    if (world < 1 || world > abcq::kMaxPeerRanks || !d_signals || !d_state || !d_err)
-        return fail(ABCQ_E_ARG, "abcq_peer_wait: bad arguments");
-    return cuda_ret(abcq::launch_peer_wait(d_signals, world, d_state, d_err, timeout_ns, (cudaStream_t)stream),
-                    "abcq_peer_wait");
+int abcq_peer_wait(void* const* peer_bases, uint32_t* const* peer_signals, int32_t world, int32_t rank,
+                   uint32_t* d_state, uint32_t* d_err, int64_t timeout_ns, void* stream) {
+    abcq::PeerOut po;
+    if (int rc = peer_out(peer_bases, peer_signals, world, rank, peer_bases ? peer_bases[rank >= 0 && rank < world ? rank : 0] : nullptr,
+                          d_state, po))
+        return rc;
+    if (!d_err) return fail(ABCQ_E_ARG, "abcq_peer_wait: err is NULL");
+    return cuda_ret(abcq::launch_peer_wait(po, d_err, timeout_ns, (cudaStream_t)stream), "abcq_peer_wait");
 }
 
 int abcq_gemv_batch(const abcq_gemv_job_t* jobs, int32_t n, void* d_ws, size_t ws_bytes, void* stream) {

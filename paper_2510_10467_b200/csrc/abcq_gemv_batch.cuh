@@ -60,9 +60,13 @@ struct Epi {
 
 // fused all-gather (abcq_gemv_batch_peer): every completed y row is also
 // stored into each peer rank's gathered buffer at the same offset
-// (symmetric layout, peer memory over NVLink), and the launch's last
-// completion block bumps this rank's epoch and publishes it in slot [rank]
-// of every peer's signal array (release, system scope)
+// (symmetric layout, peer memory over NVLink). Publication is deferred by one
+// launch: the NEXT peer launch (or abcq_peer_wait) -- once its PDL wait has
+// seen this launch complete -- fences at system scope and writes the epoch
+// into slot [rank] of every rank's signal array, from the GEMV grid's last
+// CTA (the partition's remainder: it has slack), so the ~1.5 us system-scope
+// fence is off the critical path (at the end of this launch it cost ~3 us
+// per launch with the completion counting it needed)
 constexpr int kMaxPeers = 8;
 struct Peers {
     int n;                     // ranks (0: no peer outputs)
@@ -70,9 +74,22 @@ struct Peers {
     const char* local_base;    // this rank's gathered buffer
     char* base[kMaxPeers];     // rank q's gathered buffer
     uint32_t* sig[kMaxPeers];  // rank q's signal slots [n]
-    uint32_t* state;           // this rank's [0] epoch, [32] completion blocks done (self-resetting)
-    int total_blocks;          // completion blocks of the launch
+    uint32_t* state;           // this rank's [0] epochs published, [1] a launch awaits publication
 };
+
+// publish the previous peer launch (its grid, and everything before it, has
+// completed: the caller is past its PDL wait), then mark this one pending
+__device__ __forceinline__ void peer_publish(const Peers& P, bool mark_pending) {
+    volatile uint32_t* st = P.state;
+    if (st[1]) {
+        __threadfence_system();
+        const uint32_t e = st[0] + 1u;
+        st[0] = e;
+        for (int k = 0; k < P.n; ++k)
+            asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(P.sig[k] + P.rank), "r"(e) : "memory");
+    }
+    st[1] = mark_pending ? 1u : 0u;
+}
 
 // kernel parameter: NJ job slots (1, 8 or 32 -- the smallest that fits)
 constexpr int kMaxGrid = 192;  // CTAs (one per SM)
@@ -396,17 +413,6 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
             *J.arrive = 0u;
             *J.reduced = 0u;
         }
-        if (a.pe.n) {  // fused all-gather: the launch's last completion block signals every rank
-            __threadfence_system();  // this block's peer stores (ordered by the barrier above) reach the peers
-            if (atomicAdd(a.pe.state + 32, 1u) == (uint32_t)(a.pe.total_blocks - 1)) {
-                __threadfence_system();
-                const uint32_t e = a.pe.state[0] + 1u;
-                a.pe.state[0] = e;
-                a.pe.state[32] = 0u;
-                for (int k = 0; k < a.pe.n; ++k)
-                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.pe.sig[k] + a.pe.rank), "r"(e) : "memory");
-            }
-        }
     }
     if (epi) return __syncthreads_or(last) ? j : -1;  // (block-uniform)
     return -1;
@@ -667,6 +673,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gemv_batch_kernel(const __grid_c
     pdl_wait();  // x, y and the workspace belong to the previous kernel
     pdl_launch_dependents();
     if (a.trace && tid == 0) a.trace[blockIdx.x * 8 + 7] = globaltimer();  // past the PDL wait
+    if (a.pe.n && tid == 0 && (int)blockIdx.x == a.main_ctas - 1) peer_publish(a.pe, true);
     if (a.jobs[0].nrm) {  // RMSNorm statistics of the whole input (every CTA, bitwise as add_rmsnorm)
         const Job& J = a.jobs[0];
         float v[16];
@@ -946,7 +953,6 @@ int launch_batch_nj(const BatchArgs& ba, int grid, cudaStream_t st) {
     if (a.pe.n) {
         for (int j = 0; j < ba.n_jobs; ++j)
             if (ba.jobs[j].NS <= 1) return (int)cudaErrorInvalidConfiguration;  // peer rows leave through the completion
-        a.pe.total_blocks = fused ? rblocks : sep_blocks;
     }
     cudaLaunchConfig_t cfg = {};
     const bool separate = !fused;

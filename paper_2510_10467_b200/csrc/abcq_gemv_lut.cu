@@ -227,7 +227,7 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
             }
     }
     a.prefill = g_prefill;
-    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22 || g_dbg_mode == 29 || g_dbg_mode == 32 || g_dbg_mode == 33) ? g_dbg_mode : 0;
+    a.dbg = (g_dbg_mode == 1 || g_dbg_mode == 22 || g_dbg_mode == 29 || g_dbg_mode == 32 || g_dbg_mode == 33 || g_dbg_mode == 37 || g_dbg_mode == 38) ? g_dbg_mode : 0;
     static unsigned trace_seq = 0;
     a.trace = g_trace ? g_trace + (size_t)(trace_seq++ % 16) * kTraceCtas * 8 : nullptr;
     // round trace: after the 16 launch slots, [warp][round < 32][4] stamps of CTA g_rtrace_cta
@@ -256,20 +256,22 @@ int launch_gemv_rmsnorm_out(const abcq_model_t* m, int p, const void* x, int x_d
     return launch_gemv_jobs(&m, &p, &x, &y, 1, &x_dtype, ABCQ_F16, ws, st, nullptr, &nout);
 }
 
-// consumer side of the fused all-gather: wait (one warp, lane k polls rank k's
-// slot with acquire loads at system scope) until every rank published this
-// rank's current epoch; gives up after timeout_ns and sets *err = 1 + k
-// instead of hanging
-__global__ void peer_wait_kernel(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err,
-                                 long long timeout_ns) {
-    pdl_wait();
+// consumer side of the fused all-gather: publish this rank's pending launch,
+// then wait (lane k polls rank k's slot with acquire loads at system scope)
+// until every rank published this rank's epoch; gives up after timeout_ns and
+// sets *err = 1 + k instead of hanging
+__global__ void peer_wait_kernel(const Peers P, uint32_t* err, long long timeout_ns) {
     const int k = threadIdx.x;
-    if (k >= n) return;
-    const uint32_t want = *reinterpret_cast<const volatile uint32_t*>(state);
+    pdl_wait();  // the peer launch before it has completed (PDL-launched: it ramps under that grid's tail)
+    if (k == 0) peer_publish(P, false);
+    __syncwarp();
+    if (k >= P.n) return;
+    const uint32_t want = *reinterpret_cast<const volatile uint32_t*>(P.state);
+    const uint32_t* slot = P.sig[P.rank] + k;
     const unsigned long long t0 = globaltimer();
     for (;;) {
         uint32_t v;
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sig + k) : "memory");
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(slot) : "memory");
         if ((int32_t)(v - want) >= 0) break;
         if ((long long)(globaltimer() - t0) > timeout_ns) {
             atomicCAS(err, 0u, 1u + (uint32_t)k);
@@ -279,10 +281,26 @@ __global__ void peer_wait_kernel(const uint32_t* sig, int n, const uint32_t* sta
     }
 }
 
-int launch_peer_wait(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err, long long timeout_ns,
-                     cudaStream_t st) {
-    peer_wait_kernel<<<1, 32, 0, st>>>(sig, n, state, err, timeout_ns);
-    return (int)cudaGetLastError();
+int launch_peer_wait(const PeerOut& po, uint32_t* err, long long timeout_ns, cudaStream_t st) {
+    Peers P{};
+    P.n = po.n;
+    P.rank = po.rank;
+    P.local_base = static_cast<const char*>(po.local_base);
+    for (int k = 0; k < po.n; ++k) {
+        P.base[k] = static_cast<char*>(po.base[k]);
+        P.sig[k] = po.sig[k];
+    }
+    P.state = po.state;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, peer_wait_kernel, P, err, timeout_ns);
 }
 
 }  // namespace abcq

@@ -40,8 +40,7 @@ struct PeerOut {
     uint32_t* sig[kMaxPeerRanks];
     uint32_t* state;
 };
-int launch_peer_wait(const uint32_t* sig, int n, const uint32_t* state, uint32_t* err, long long timeout_ns,
-                     cudaStream_t st);
+int launch_peer_wait(const PeerOut& po, uint32_t* err, long long timeout_ns, cudaStream_t st);
 int lut_max_jobs();
 
 // fused input mode of the persistent GEMV: input = f16(f16(x + residual) * inv_rms * norm_w),

@@ -178,11 +178,13 @@ class PeerGather:
         return PeerGemvPlan(self, jobs)
 
     def wait(self, stream=None, timeout_s: float = 2.0) -> None:
-        """Enqueue: block the stream until every rank's rows of the latest
-        launch are in this rank's buffer (bounded: `err` = 1 + the late rank)."""
+        """Enqueue: publish this rank's latest launch, then block the stream
+        until every rank's rows of its latest launch are in this rank's buffer
+        (bounded: `err` = 1 + the late rank). Every rank calls it after the
+        same launch."""
         from .device_model import _stream_handle
-        sig = int(self._sigs[self.rank])
-        self._lib.check(self._lib.lib().abcq_peer_wait(sig, self.world, self.state.data_ptr(), self.err.data_ptr(),
+        self._lib.check(self._lib.lib().abcq_peer_wait(self._bases, self._sigs, self.world, self.rank,
+                                                       self.state.data_ptr(), self.err.data_ptr(),
                                                        int(timeout_s * 1e9), _stream_handle(stream)),
                         "abcq_peer_wait")
 

@@ -810,8 +810,9 @@ def test_fused_peer_allgather_world1(P):
 def test_fused_peer_stores_two_buffers_one_gpu(P):
     """The peer-store data path on one GPU: a 2-'rank' launch whose 'peer'
     buffer is a second local buffer -- rank 0's rows land in both buffers at
-    the same offsets (bitwise), the epoch is published in both signal arrays,
-    and the C-ABI argument checks hold (peer_bases[rank] must be local)."""
+    the same offsets (bitwise), the wait publishes the epoch in both signal
+    arrays and times out (err, no hang) on the 'rank' that never runs, and the
+    C-ABI argument checks hold (peer_bases[rank] must be local)."""
     import ctypes as C
 
     from paper_2510_10467_b200 import _lib
@@ -832,13 +833,19 @@ def test_fused_peer_stores_two_buffers_one_gpu(P):
     bases = (C.c_void_p * 2)(buf[0].data_ptr(), buf[1].data_ptr())
     sigs = (C.c_void_p * 2)(sig[0].data_ptr(), sig[1].data_ptr())
     sh = torch.cuda.current_stream().cuda_stream
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
     for it in (1, 2):
         _lib.check(L.abcq_gemv_batch_peer(plan.arr, plan.n, buf[0].data_ptr(), buf[0].numel() * 2, bases, sigs, 2, 0,
                                           state.data_ptr(), ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch_peer")
         torch.cuda.synchronize()
         want = gemv_batch([(dm, 3, x, torch.empty(dm.rows, device="cuda", dtype=torch.float16)) for dm in dms])
         assert torch.equal(buf[0][:R], torch.cat(want)) and torch.equal(buf[1][:R], buf[0][:R])
-        assert int(state[0]) == it and int(sig[0][0]) == it and int(sig[1][0]) == it
+        assert int(state[0]) == it - 1  # this launch is still pending: published by the next one / the wait
+        # the wait publishes it to both signal arrays, then times out on 'rank 1' (nobody runs it): err = 1 + 1
+        err.zero_()
+        _lib.check(L.abcq_peer_wait(bases, sigs, 2, 0, state.data_ptr(), err.data_ptr(), 2_000_000, sh), "abcq_peer_wait")
+        torch.cuda.synchronize()
+        assert int(state[0]) == it and int(sig[0][0]) == it and int(sig[1][0]) == it and int(err) == 2
     assert not buf[1][R:].any()  # rank 1's rows: nobody wrote them
     swapped = (C.c_void_p * 2)(buf[1].data_ptr(), buf[0].data_ptr())
     with pytest.raises(P.UsageError):

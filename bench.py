@@ -365,6 +365,11 @@ def run_gpu(args):
         except Exception as exc:  # noqa: BLE001
             peer = peer_plan = None
             ag_mode = f"nccl (fused peer all-gather unavailable: {str(exc)[:100]})"
+        ok = torch.tensor([1 if peer is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if peer is not None and int(ok.item()) == 0:
+            peer = peer_plan = None
+            ag_mode = "nccl (fused peer all-gather unavailable on another rank)"
     if mp_reserve and ag_mode == "peer":  # no collective kernel beside the GEMV grid
         P.set_reserved_sms(0)
         mp_reserve = 0
@@ -1050,7 +1055,10 @@ def config5_row_sharded(ctx, args, peak):
     # fused all-gather buffers (one symmetric buffer per layer, rank r's rows
     # at r * per-rank rows) when a process group exists
     peers, peer_plans = [], {}
-    if dist.is_initialized() and all(e is not None for e in engines):
+    if dist.is_initialized():
+        usable = torch.tensor([1 if all(e is not None for e in engines) else 0], device=ctx.dev)
+        dist.all_reduce(usable, op=dist.ReduceOp.MIN)
+    if dist.is_initialized() and int(usable.item()) == 1:
         try:
             from paper_2510_10467_b200.parallel import PeerGather
             for li, (name, r, k) in enumerate(LAYERS_70B):
@@ -1062,6 +1070,11 @@ def config5_row_sharded(ctx, args, peak):
         except Exception as exc:  # noqa: BLE001
             peers, peer_plans = [], {}
             res["fused_allgather"] = f"unavailable: {str(exc)[:100]}"
+        ok = torch.tensor([1 if peers else 0], device=ctx.dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if peers and int(ok.item()) == 0:
+            peers, peer_plans = [], {}
+            res["fused_allgather"] = "unavailable on another rank"
     for p in (2, 4):
         def local_all():
             for e in engines:

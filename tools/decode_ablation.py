@@ -21,5 +21,19 @@ for name in ("qkv", "o", "gu", "down"):
     out["skip_" + name] = round(time_step(qm, 20), 4)
     for mats, dm in zip(qm.layers, saved):
         mats[name] = dm
+# the harness ops: attention (RoPE + KV append + split-L attention + combine) and add+RMSNorm
+attn = qm.attn
+qm.attn = lambda li, q, k, v: attn.out
+out["skip_attention"] = round(time_step(qm, 20), 4)
+qm.attn = attn
+norm = D.add_rmsnorm
+D.add_rmsnorm = lambda *a, **k: None
+out["skip_add_rmsnorm"] = round(time_step(qm, 20), 4)
+D.add_rmsnorm = norm
+lm = qm.lm_head
+qm.lm_head = lm[:16].contiguous()
+qm.logits = qm.logits[:16]
+out["skip_lm_head"] = round(time_step(qm, 20), 4)
+qm.lm_head = lm
 out["full2"] = round(time_step(qm, 20), 4)
 print(json.dumps(out))

@@ -158,7 +158,7 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
  * x: (cols) in x_dtype, 16-byte aligned (TILED); y: (rows) in y_dtype.
  * TILED layout -> an sm_100a LUT kernel: the cluster kernel (split-K through
  * distributed shared memory, one launch, no workspace use) for latency-bound
- * GEMVs (<= 24 MiB of planes and <= 32 column slices), else the persistent
+ * GEMVs (<= 32 MiB of planes and <= 32 column slices), else the persistent
  * streaming kernel; ROWMAJOR layout (any group size) -> the generic kernel.
  * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials + self-
  * resetting completion counters): zero-filled once before first use; may

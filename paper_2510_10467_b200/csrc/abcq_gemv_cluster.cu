@@ -162,15 +162,17 @@ static int launch_xy(const Args& a, int sd, bool asym, int smem, int W, cudaStre
 
 bool cluster_supports(const abcq_model_t* m, int p) {
     if (m->layout != ABCQ_LAYOUT_TILED || p < 1 || p > ABCQ_MAX_PLANES || g_dbg_mode == 23) return false;
-    // dispatch (tools/cl_probe.py, back-to-back single launches, B200): the
-    // cluster kernel wins while a GEMV is latency-bound -- up to ~24 MB of plane
-    // bytes and <= 2 slices per CTA at C = 16; larger GEMVs stream better
-    // through the persistent batch kernel (more CTAs, deeper rings)
+    // dispatch (tools/cl_probe.py, tools/per_shape_ab.py, back-to-back single
+    // launches, B200): the cluster kernel wins while a GEMV is latency-bound --
+    // up to 32 MiB of plane bytes (14336 x 4096 at p = 4: 12.0 vs 13.4 us;
+    // the decode step's 28672 x 4096 gate/up at p = 2) and <= 2 slices per CTA
+    // at C = 16; larger GEMVs stream better through the persistent batch
+    // kernel (the decode step's gate/up at p = 3 / 4)
     // (27: every single GEMV through the cluster kernel -- test coverage;
     //  28: any size up to 32 slices -- experiments)
     if (g_dbg_mode != 27) {
         const int64_t plane_bytes = (int64_t)p * tiled_plane_bytes(m->rows, m->cols);
-        if (n_slices(m->cols) > 32 || (g_dbg_mode != 28 && plane_bytes > (int64_t)24 * 1024 * 1024)) return false;
+        if (n_slices(m->cols) > 32 || (g_dbg_mode != 28 && plane_bytes > (int64_t)32 * 1024 * 1024)) return false;
     }
     cl::Geom g;
     return cl::plan(m, p, g);

@@ -136,7 +136,11 @@ class _Attention:
         return self.out
 
 
-PERSISTENT_QKV_O = True  # (tools/decode_ab.py --cluster-qkv-o measures the alternative)
+# q/k/v and o: the cluster kernel (abcq_gemv) -- after round 2's changes to
+# the persistent kernel it measured faster for them inside the step at every
+# p (tools/decode_paths_ab.py: p2/p3/p4 2.069/2.304/2.420 vs 2.104/2.326/2.479
+# ms/token); True routes them through the persistent batch kernel
+PERSISTENT_QKV_O = False
 
 
 def _persistent(m, p, x, out):
@@ -242,10 +246,7 @@ class QuantizedLlamaStep:
         resid = None
         cur, nxt = self.x, self.x_alt  # an even number of fused norms per step: it ends in self.x
         for li, mats in enumerate(self.layers):
-            # q/k/v and o through the persistent batch kernel even as single jobs:
-            # between the step's other kernels it measured faster than the
-            # latency-path cluster kernel abcq_gemv takes for these shapes
-            # (p3: 2.19 vs 2.25 ms/token, tools/decode_ab.py)
+            # q/k/v and o: see PERSISTENT_QKV_O
             new = self._norm_linear(mats, "qkv", cur, nxt, resid, self.norm_w[li][0], self.qkv)
             cur, nxt = (new, cur) if new is not cur else (cur, nxt)
             a = self.attn(li, self.q, self.k, self.v)

@@ -223,10 +223,13 @@ def test_argmax_matches_torch(n):
         assert int(out) == int(torch.argmax(x)), (n, trial)
 
 
-def test_quantized_step_fused_norm_equals_separate_add_rmsnorm():
+def test_quantized_step_fused_norm_equals_separate_add_rmsnorm(monkeypatch):
     """add + RMSNorm inside the q/k/v and gate/up GEMVs (abcq_gemv_add_rmsnorm)
-    == the separate add_rmsnorm launch: bitwise equal step state and token."""
+    == the separate add_rmsnorm launch: bitwise equal step state and token
+    (the separate path's GEMVs on the same persistent kernel)."""
+    import paper_2510_10467_b200.decode as D
     from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    monkeypatch.setattr(D, "PERSISTENT_QKV_O", True)
     cfg = LlamaConfig(layers=3, vocab=1000)
     m = QuantizedLlamaStep(cfg, p=3, ctx=64, fuse_norm=True)
     x0 = m.x.clone()
@@ -270,10 +273,13 @@ def test_gemv_add_rmsnorm_matches_separate_ops():
         dm.gemv_add_rmsnorm(3, x, r, w, 1e-5, out=y, x_out=x)   # x_out aliases x
 
 
-def test_quantized_step_norm_out_equals_separate_add_rmsnorm():
+def test_quantized_step_norm_out_equals_separate_add_rmsnorm(monkeypatch):
     """add + RMSNorm as the o / down GEMVs' epilogue (abcq_gemv_rmsnorm_out,
-    fuse_norm_out=True) == the separate launches: bitwise equal step state and token."""
+    fuse_norm_out=True) == the separate launches: bitwise equal step state and
+    token (the separate path's GEMVs on the same persistent kernel)."""
+    import paper_2510_10467_b200.decode as D
     from paper_2510_10467_b200.decode import LlamaConfig, QuantizedLlamaStep
+    monkeypatch.setattr(D, "PERSISTENT_QKV_O", True)
     cfg = LlamaConfig(layers=3, vocab=1000)
     m = QuantizedLlamaStep(cfg, p=3, ctx=64, fuse_norm_out=True)
     assert m.fuse_norm_out

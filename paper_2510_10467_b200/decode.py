@@ -157,7 +157,7 @@ class QuantizedLlamaStep:
 
     def __init__(self, cfg: LlamaConfig = LlamaConfig(), p: int = 3, p_lo: int = 2, p_hi: int = 4,
                  ctx: int = 1024, device=None, seed: int = 0, fuse_glu: bool = True, stack_rows: bool = True,
-                 fuse_norm: bool = False, fuse_norm_out: bool = False):
+                 fuse_norm: bool | None = None, fuse_norm_out: bool = False):
         self.cfg, self.p, self.fuse_glu, self.stack_rows = cfg, p, fuse_glu, stack_rows
         # fuse_norm_out: the add + RMSNorm after the o and down projections runs
         # as those GEMVs' epilogue (abcq_gemv_rmsnorm_out: the block that
@@ -171,11 +171,13 @@ class QuantizedLlamaStep:
             raise ValueError("fuse_norm (GEMV input side) and fuse_norm_out (output side) are exclusive")
         self.fuse_norm_out = fuse_norm_out and fuse_glu and stack_rows
         # fuse_norm: add + RMSNorm formed inside the q/k/v and gate/up GEMVs'
-        # table builds (abcq_gemv_add_rmsnorm, bitwise equal to the separate
-        # launch). Off by default: measured 2.14 vs 2.11 ms/token at p=3 -- every
-        # CTA then waits for the whole-vector statistics before its tables,
-        # while the separate launch overlaps the GEMV's weight prefetch (PDL)
-        self.fuse_norm = fuse_norm
+        # table builds (abcq_gemv_add_rmsnorm on the persistent kernel, bitwise
+        # equal to the separate launch + that GEMV). On by default (unless
+        # fuse_norm_out): with round 2's persistent-kernel schedule it measures
+        # p2/p3/p4 1.991/2.147/2.300 vs 1.994/2.337/2.434 ms/token for the
+        # separate launch (tools/decode_norm_ab.py, medians of 3 alternated
+        # rounds; early in round 2 it measured 2.14 vs 2.11 at p=3, the other way)
+        self.fuse_norm = (not fuse_norm_out) if fuse_norm is None else fuse_norm
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         gen = torch.Generator(device=self.device).manual_seed(seed)
         self.layers = []

@@ -625,10 +625,14 @@ def step_variants(ctx, models, xs, ys, peak):
     and one launch per precision; each with its roofline fraction."""
     gemv_batch, st = ctx.gemv_batch, ctx.stream
 
-    def grouped(groups):
+    def grouped(groups):  # a group of one is a single GEMV (abcq_gemv: the cluster kernel where it wins)
         for pi, p in enumerate(PRECISIONS):
             for grp in groups:
-                gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], st)
+                if len(grp) == 1:
+                    m = models[pi][grp[0]]
+                    m.gemv(p, xs[m.cols], out=ys[pi][grp[0]], stream=st)
+                else:
+                    gemv_batch([(models[pi][li], p, xs[models[pi][li].cols], ys[pi][li]) for li in grp], st)
 
     def singles():
         for pi, p in enumerate(PRECISIONS):
@@ -646,7 +650,8 @@ def step_variants(ctx, models, xs, ys, peak):
             "roofline_decoder_grouped": {"bound": "hbm", "achieved": res["decoder_grouped"]["GBps"], "peak": peak,
                                          "unit": "GB/s", "frac": res["decoder_grouped"]["roofline_frac"],
                                          "what": "the step's 21 GEMVs as a decoder issues them: 4 launches per "
-                                                 "precision ([q,k,v] [o] [gate,up] [down], each a batched launch)"},
+                                                 "precision ([q,k,v] and [gate,up] batched launches, [o] and [down] "
+                                                 "single GEMVs)"},
             "roofline_single_launch": {"bound": "hbm", "achieved": res["single_launch_per_gemv"]["GBps"],
                                        "peak": peak, "unit": "GB/s",
                                        "frac": res["single_launch_per_gemv"]["roofline_frac"],

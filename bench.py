@@ -400,6 +400,9 @@ def run_gpu(args):
             step_mp(i) if mp else step_launches()
         if mp:
             mp_drain()
+        if peer_plan is not None:  # (its workspace allocated outside the graph capture)
+            for i in range(max(args.warmup, 3)):
+                peer_plan.launch(stream)
     torch.cuda.synchronize()
 
     side = torch.cuda.Stream(device=dev) if mp else None

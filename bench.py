@@ -790,15 +790,7 @@ def e2e_section(ctx, models, xs, all_jobs, args):
             H["plans"].append(P.GemvBatchPlan([(models[pi][li], p, dx[models[pi][li].cols], dys[n])
                                                for n, (pi, p, li) in enumerate(all_jobs)]))
         halves.append(H)
-    # every plan's launches are ordered on the one compute stream: they share
-    # ONE split-K workspace (its counters self-reset), so the step's partials
-    # stay in one L2-resident region instead of rotating over 2 * E2E_GROUP
-    if os.environ.get("ABCQ_E2E_SHARED_WS", "1") == "1":
-        shared = torch.zeros(halves[0]["plans"][0].need, dtype=torch.uint8, device=dev)
-        sh = st.cuda_stream
-        for H in halves:
-            for plan in H["plans"]:
-                plan._ws[sh] = shared
+    # (every plan shares the compute stream's one split-K workspace: device_model.stream_workspace)
     ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "comp", "out")}  # per group parity
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     cnt = {"h2d": 0, "d2h": 0}

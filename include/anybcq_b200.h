@@ -160,9 +160,12 @@ int abcq_lut_build(const void* d_x, int32_t x_dtype, int32_t cols, int32_t chunk
  * distributed shared memory, one launch, no workspace use) for latency-bound
  * GEMVs (<= 32 MiB of planes and <= 32 column slices), else the persistent
  * streaming kernel; ROWMAJOR layout (any group size) -> the generic kernel.
- * Workspace: >= abcq_gemv_workspace_bytes() (split-K partials + self-
- * resetting completion counters): zero-filled once before first use; may
- * not be shared by calls running concurrently (one workspace per stream).  */
+ * Workspace: >= abcq_gemv_workspace_bytes() (self-resetting completion
+ * counters at offset 0, then the split-K partials): zero-filled once before
+ * first use; ONE workspace (of the largest size needed) may serve every
+ * model's abcq_gemv / abcq_gemv_batch launched in order on a stream -- and
+ * should: the partials then stay L2-resident instead of spreading over many
+ * buffers -- but not calls running concurrently (one workspace per stream). */
 int abcq_gemv_workspace_bytes(const abcq_model_t* m, size_t* out_bytes);
 int abcq_gemv(const abcq_model_t* m, int32_t p, const void* d_x, int32_t x_dtype, void* d_y,
               int32_t y_dtype, void* d_workspace, size_t workspace_bytes, void* stream);
@@ -197,9 +200,9 @@ int abcq_gemv_rmsnorm_out(const abcq_model_t* m, int32_t p, const void* d_x, int
  * streaming kernel, also for n_jobs == 1 (abcq_gemv instead takes the
  * latency-path cluster kernel for small GEMVs). All jobs: TILED layout,
  * the same x/y/scale dtypes and mode; n_jobs <= abcq_gemv_batch_max_jobs().
- * Workspace: abcq_gemv_batch_workspace_bytes (the jobs' split-K partials,
- * then per-job self-resetting counters): zero-filled once per stream AND
- * per job-list layout (the counters' offset depends on the jobs' shapes).   */
+ * Workspace: abcq_gemv_batch_workspace_bytes (per-job self-resetting
+ * counters at offset 0, then the jobs' split-K partials): as for abcq_gemv,
+ * one zero-filled workspace per stream serves every job list.               */
 typedef struct abcq_gemv_job {
     const abcq_model_t* model;
     int32_t p;

@@ -31,9 +31,13 @@ static size_t partial_bytes(const abcq_model_t* m) {
 constexpr int kCounterStride = 32;  // one 128-byte line per counter: spinning readers and arrivals of
                                     // different jobs never share a line
 constexpr size_t kCounterBytes = 2 * kMaxJobs * kCounterStride * sizeof(uint32_t);  // per job: CTA arrivals, reduce blocks done
+static_assert(kCounterBytes % 256 == 0, "partials after the counters stay 256-byte aligned");
 
-// workspace of a job list: every split job's partials, then (if any job is
-// split) the self-resetting per-job counters -- zero-filled once before use
+// workspace of a job list: (if any job is split) the self-resetting per-job
+// counters FIRST -- at the same offset for every job list, so one zero-filled
+// workspace serves every model and batch launched in order on a stream
+// (partials are always written before they are read) -- then every split
+// job's partials
 size_t lut_jobs_workspace_bytes(const abcq_model_t* const* models, int n) {
     size_t tot = 0;
     for (int j = 0; j < n; ++j) tot += partial_bytes(models[j]);
@@ -94,7 +98,8 @@ int launch_gemv_jobs(const abcq_model_t* const* models, const int* ps, const voi
     int64_t units = 0;
     size_t part_total = 0;
     for (int j = 0; j < n; ++j) part_total += partial_bytes(models[j]);
-    uint32_t* counters = part_total ? reinterpret_cast<uint32_t*>(w + part_total) : nullptr;
+    uint32_t* counters = part_total ? reinterpret_cast<uint32_t*>(w) : nullptr;
+    if (part_total) w += kCounterBytes;  // (kCounterBytes: a multiple of 256, partials stay aligned)
     for (int j = 0; j < n; ++j) {
         make_job(a.jobs[j], models[j], ps[j], xs[j], ys[j], w);
         a.jobs[j].glu = x_dtypes[j] == ABCQ_F16_SILU_GLU;

@@ -212,7 +212,8 @@ class PeerGemvPlan:
         sh = _stream_handle(stream)
         ws = b._ws.get(sh)
         if ws is None:
-            ws = b._ws[sh] = torch.zeros(b.need, dtype=torch.uint8, device=b.device)
+            from .device_model import stream_workspace
+            ws = b._ws[sh] = stream_workspace(b.device, sh, b.need)
         nbytes = g.buffer.numel() * g.buffer.element_size()
         g._lib.check(b._L.abcq_gemv_batch_peer(b.arr, b.n, g.buffer.data_ptr(), nbytes, g._bases, g._sigs, g.world,
                                                g.rank, g.state.data_ptr(), ws.data_ptr(), ws.numel(), sh),

@@ -851,3 +851,34 @@ def test_fused_peer_stores_two_buffers_one_gpu(P):
     with pytest.raises(P.UsageError):
         _lib.check(L.abcq_gemv_batch_peer(plan.arr, plan.n, buf[0].data_ptr(), buf[0].numel() * 2, swapped, sigs, 2, 0,
                                           state.data_ptr(), ws.data_ptr(), ws.numel(), sh), "abcq_gemv_batch_peer")
+
+
+def test_stream_workspace_shared_and_grown(P):
+    """One split-K workspace per (device, stream) serves every model and batch
+    launched in order on it (counters at offset 0 of every layout): models of
+    different sizes interleaved on one stream -- the workspace growing under
+    them, the replaced buffer kept alive for whoever cached it -- give
+    bitwise the results of the same calls each on a fresh stream."""
+    from paper_2510_10467_b200 import device_model as DMm
+    st = torch.cuda.Stream()
+    small = P.DeviceModel.from_model(synth_model(P, 512, 4096, 2, 4, seed=1), scale_dtype="f16")
+    big = P.DeviceModel.from_model(synth_model(P, 8192, 8192, 2, 4, seed=2), scale_dtype="f16")
+    xs = {c: torch.from_numpy(O.random_gaussian(1, c, seed=c).ravel()).cuda().half() for c in (4096, 8192)}
+    calls = [(small, 2), (big, 3), (small, 4), (big, 2), (small, 3)]
+    want = []
+    for dm, p in calls:  # each on its own fresh stream (its own workspace)
+        s2 = torch.cuda.Stream()
+        with torch.cuda.stream(s2):
+            want.append(DMm.gemv_batch([(dm, p, xs[dm.cols], torch.empty(dm.rows, device="cuda",
+                                                                            dtype=torch.float16))], s2)[0])
+        torch.cuda.synchronize()
+    n_old = len(DMm._STREAM_WS_OLD)
+    got = []
+    with torch.cuda.stream(st):
+        for dm, p in calls:
+            got.append(DMm.gemv_batch([(dm, p, xs[dm.cols], torch.empty(dm.rows, device="cuda",
+                                                                           dtype=torch.float16))], st)[0])
+    torch.cuda.synchronize()
+    assert len(DMm._STREAM_WS_OLD) >= n_old + 1  # it grew under the small model's first call
+    for g, w in zip(got, want):
+        assert torch.equal(g, w)

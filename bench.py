@@ -563,6 +563,8 @@ def run_gpu(args):
             out["config3"] = config3(ctx)
         if want("config4"):
             out["config4"] = config4(ctx, args)
+        if want("loader"):
+            out["loader"] = loader_section(ctx, args)
         if want("quantizer"):
             out["quantizer"] = quantizer_section(ctx, args)
     if mp:
@@ -1156,6 +1158,53 @@ def config5_row_sharded(ctx, args, peak):
     return res
 
 
+def loader_section(ctx, args):
+    """an .abcq container (14336 x 4096, p = 2..4, f16
+    scales -- one Llama-3-8B gate layer) to a GPU-resident model through
+    ProgressiveLoader: the host mmap -> pinned -> device upload and the tiled
+    repack, time to the first servable precision (planes 1..p_lo + set p_lo:
+    a GEMV at p_lo can launch) and to the whole model, wall time with the
+    device synchronised; file bytes / time."""
+    torch = ctx.torch
+    import tempfile
+
+    from paper_2510_10467_b200.container import ProgressiveLoader, serialize
+    from paper_2510_10467_b200.model import BitPlaneSet, MultiPrecisionModel, QuantConfig, ScaleTensor
+    from paper_2510_10467_b200.tensor_io import random_words
+
+    rows, cols, p_lo, p_hi = 14336, 4096, 2, 4
+    rng = np.random.default_rng(5)
+    words = random_words(p_hi, rows, cols, seed=9)
+    sets = {p: ScaleTensor((0.01 + 0.1 * np.abs(rng.standard_normal((p, rows, cols // 128)))).astype(np.float32),
+                           None, 128) for p in range(p_lo, p_hi + 1)}
+    model = MultiPrecisionModel(BitPlaneSet(p_hi, rows, cols, words), sets, p_lo, p_hi, QuantConfig(128))
+    x = torch.randn(cols, device=ctx.dev).half()
+    res = {}
+    with tempfile.TemporaryDirectory() as td:
+        path = str(Path(td) / "layer.abcq")
+        serialize(model, path, scale_width=2)
+        nbytes = os.path.getsize(path)
+        for rep in range(3):  # (first: allocator / module warm-up)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ld = ProgressiveLoader(path, device=ctx.dev)
+            ld.load_level()
+            y = ld.model.gemv(p_lo, x)  # ordered after its level's upload on the device
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ld.load_all()
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            ld.close()
+            del ld, y
+        res = {"shape": [rows, cols], "precisions": [p_lo, p_hi], "file_bytes": nbytes,
+               "first_gemv_s": round(t1 - t0, 4), "all_levels_s": round(t2 - t0, 4),
+               "GBps_file": round(nbytes / (t2 - t0) / 1e9, 2),
+               "what": "ProgressiveLoader: header + CRC check, planes 1..p_lo + set p_lo uploaded and one GEMV at "
+                       "p_lo served, then the remaining levels; wall seconds, device synchronised"}
+    return res
+
+
 def quantizer_section(ctx, args):
     """The GPU quantizer: build_multiprecision 2:4,
     group 128, cycles 1 (the reference CLI's bench-suite fit, cli.py:150-152)
@@ -1309,7 +1358,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
     ap.add_argument("--sections", default="", help="comma list of the extra sections to run (default: all): "
-                    "variants,per_shape,fp16,batched8,e2e,config1,config3,config4,config5,quantizer")
+                    "variants,per_shape,fp16,batched8,e2e,config1,config3,config4,config5,loader,quantizer")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

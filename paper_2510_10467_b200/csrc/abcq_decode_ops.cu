@@ -287,16 +287,44 @@ __global__ void rope_attn_decode_fused(const __half* __restrict__ q, const __hal
     // attn_decode_combine's arithmetic for the g heads of this kv head: warp w, dims 4l..4l+3
     const float* ph = part + (size_t)h * splits * kPartStride;
     float M = -INFINITY;
-    for (int t = 0; t < splits; ++t) M = fmaxf(M, __ldcg(ph + t * kPartStride));
     float num[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
-    for (int t = 0; t < splits; ++t) {
-        const float w = __expf(__ldcg(ph + t * kPartStride) - M);
-        den = fmaf(w, __ldcg(ph + t * kPartStride + 1), den);
-        const float4 a = __ldcg(reinterpret_cast<const float4*>(ph + t * kPartStride + 4 + 4 * lane));
-        num[0] = fmaf(w, a.x, num[0]);
-        num[1] = fmaf(w, a.y, num[1]);
-        num[2] = fmaf(w, a.z, num[2]);
-        num[3] = fmaf(w, a.w, num[3]);
+    if (splits <= 32) {
+        // every split's (m, l) in flight at once (lane t holds split t), the max
+        // by shuffles (exact, order-free), then the same ascending fmaf chains
+        // as below with the acc rows loaded 8 splits at a time: a few L2 round
+        // trips instead of one per split -- bitwise the same result
+        const float mt = lane < splits ? __ldcg(ph + lane * kPartStride) : -INFINITY;
+        const float lt = lane < splits ? __ldcg(ph + lane * kPartStride + 1) : 0.f;
+        M = warp_max(mt);
+        const float wt = lane < splits ? __expf(mt - M) : 0.f;
+        for (int t0 = 0; t0 < splits; t0 += 8) {
+            float4 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (t0 + u < splits)
+                    a[u] = __ldcg(reinterpret_cast<const float4*>(ph + (t0 + u) * kPartStride + 4 + 4 * lane));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (t0 + u >= splits) break;
+                const float w = __shfl_sync(0xffffffffu, wt, t0 + u);
+                den = fmaf(w, __shfl_sync(0xffffffffu, lt, t0 + u), den);
+                num[0] = fmaf(w, a[u].x, num[0]);
+                num[1] = fmaf(w, a[u].y, num[1]);
+                num[2] = fmaf(w, a[u].z, num[2]);
+                num[3] = fmaf(w, a[u].w, num[3]);
+            }
+        }
+    } else {
+        for (int t = 0; t < splits; ++t) M = fmaxf(M, __ldcg(ph + t * kPartStride));
+        for (int t = 0; t < splits; ++t) {
+            const float w = __expf(__ldcg(ph + t * kPartStride) - M);
+            den = fmaf(w, __ldcg(ph + t * kPartStride + 1), den);
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(ph + t * kPartStride + 4 + 4 * lane));
+            num[0] = fmaf(w, a.x, num[0]);
+            num[1] = fmaf(w, a.y, num[1]);
+            num[2] = fmaf(w, a.z, num[2]);
+            num[3] = fmaf(w, a.w, num[3]);
+        }
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) out[(size_t)h * d + 4 * lane + j] = __float2half_rn(num[j] / den);

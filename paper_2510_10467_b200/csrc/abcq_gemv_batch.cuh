@@ -362,19 +362,23 @@ __device__ __forceinline__ int reduce_rows(const KArgs<NJ>& a, int blk) {
     for (int q = 0; q < RPT; ++q)
 #pragma unroll
         for (int u = 0; u < CPT; ++u) c[q][u] = 0.f;
-    for (int b0 = 0; b0 < nterm; b0 += 16 / CPT) {  // 16 loads per row in flight
-        float v[RPT][16];
+    // loads per row in flight: 32 for one row per thread (the trailing CTAs of
+    // single GEMVs: a 56-slice down projection's sums in one L2 round trip),
+    // 16 for the separate kernel's two rows per thread
+    constexpr int KB = RPT == 1 ? 32 : 16;
+    for (int b0 = 0; b0 < nterm; b0 += KB / CPT) {
+        float v[RPT][KB];
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {  // chain sub*CPT + k%CPT, term b0 + k/CPT
+            for (int k = 0; k < KB; ++k) {  // chain sub*CPT + k%CPT, term b0 + k/CPT
                 const int term = b0 + k / CPT, s = term * 4 + sub * CPT + k % CPT;
                 v[q][k] = (term < nterm && s < J.NS) ? __ldcg(pp[q] + s * kTileRows) : 0.f;
             }
 #pragma unroll
         for (int q = 0; q < RPT; ++q)
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
+            for (int k = 0; k < KB; ++k)
                 if (b0 + k / CPT < nterm) c[q][k % CPT] += v[q][k];
     }
 #pragma unroll

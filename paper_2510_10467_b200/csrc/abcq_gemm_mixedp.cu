@@ -23,6 +23,8 @@
 // read straight from the staging buffer and un-rotated in registers.
 // This is a dense contraction (2*B flops per weight bit), hence tensor cores;
 // the batch-1 path is the LUT kernel.
+#include <type_traits>
+
 #include "abcq_common.cuh"
 #include "abcq_internal.h"
 
@@ -234,26 +236,43 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                     uint32_t xa[8][4];            // A fragments of this group's 8 k-steps
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) ldmatrix_x4(xa[kk], &S.xs[xrow][gg * 128 + kk * 16 + xcol]);
-                    for (int ii = 0; ii < np; ++ii) {
-                        const int i = i0 + ii;
-                        // rows g and g+8 of the tile: their 16 group bytes (lane chunk gg*16 + row)
-                        uint32_t rowb[2][4];
-                        unrotate16<false>(stage[warp][buf][ii][gg * 16 + g], rk1, rsh, rowb[0]);
-                        unrotate16<true>(stage[warp][buf][ii][gg * 16 + g + 8], rk1, rsh, rowb[1]);
-                        const ST* scs = reinterpret_cast<const ST*>(&S.sc[warp][buf][ii][0][0]);  // [set][32]
-                        float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+                    // planes two at a time: four independent MMA chains per warp
+                    // (the per-warp dependency chain, not any one pipe, bounds this
+                    // kernel -- DESIGN.md §3.3); scaling in plane order as before
+                    auto planes_n = [&](auto npl_c, int ii0) {
+                        constexpr int NPL = decltype(npl_c)::value;
+                        uint32_t rowb[NPL][2][4];
+                        float c[NPL][2][4];
+#pragma unroll
+                        for (int pl = 0; pl < NPL; ++pl) {
+                            // rows g and g+8 of the tile: their 16 group bytes (lane chunk gg*16 + row)
+                            unrotate16<false>(stage[warp][buf][ii0 + pl][gg * 16 + g], rk1, rsh, rowb[pl][0]);
+                            unrotate16<true>(stage[warp][buf][ii0 + pl][gg * 16 + g + 8], rk1, rsh, rowb[pl][1]);
+#pragma unroll
+                            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) c[pl][q][j] = 0.f;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
 #pragma unroll
-                            for (int q = 0; q < 2; ++q) {  // q: weight rows g (0-7 tile) / g+8 (8-15 tile)
-                                // weight bits 4t..4t+3 of k-step kk (see the X permutation), as
-                                // the byte offset 8 * nibble of its table entry
-                                const uint32_t w = rowb[q][kk >> 1];
-                                const uint32_t off = (kk & 1) ? (w >> (13 + 4 * t)) & 0x78u : ((w << 3) >> (4 * t)) & 0x78u;
-                                const uint2 bf = lds64(nib_base | off);
-                                mma16816(c[q], xa[kk], bf.x, bf.y);
-                            }
+                            for (int pl = 0; pl < NPL; ++pl)
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) {  // q: weight rows g (0-7 tile) / g+8 (8-15 tile)
+                                    // weight bits 4t..4t+3 of k-step kk (see the X permutation), as
+                                    // the byte offset 8 * nibble of its table entry
+                                    const uint32_t w = rowb[pl][q][kk >> 1];
+                                    const uint32_t off =
+                                        (kk & 1) ? (w >> (13 + 4 * t)) & 0x78u : ((w << 3) >> (4 * t)) & 0x78u;
+                                    const uint2 bf = lds64(nib_base | off);
+                                    mma16816(c[pl][q], xa[kk], bf.x, bf.y);
+                                }
                         }
+#pragma unroll
+                        for (int pl = 0; pl < NPL; ++pl) {
+                            const int ii = ii0 + pl, i = i0 + ii;
+                            const float (&cc)[2][4] = c[pl];
+                            const ST* scs = reinterpret_cast<const ST*>(&S.sc[warp][buf][ii][0][0]);  // [set][32]
                         // scale: C[q] holds requests {g, g+8} x rows {q*8 + 2t, q*8 + 2t + 1};
                         // staged sets are zero beyond their precision, so no masking
                         if (!a.overflow) {
@@ -262,8 +281,8 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
 #pragma unroll
                                 for (int rq = 0; rq < 2; ++rq) {
                                     const float2 av = ld_scale2<ST>(scs + (rq ? soff1 : soff0) + gg * 16 + q * 8 + 2 * t);
-                                    y[rq][q * 2] = fmaf(av.x, c[q][rq * 2], y[rq][q * 2]);
-                                    y[rq][q * 2 + 1] = fmaf(av.y, c[q][rq * 2 + 1], y[rq][q * 2 + 1]);
+                                    y[rq][q * 2] = fmaf(av.x, cc[q][rq * 2], y[rq][q * 2]);
+                                    y[rq][q * 2 + 1] = fmaf(av.y, cc[q][rq * 2 + 1], y[rq][q * 2 + 1]);
                                 }
                         } else {
 #pragma unroll
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                                             av = to_f32<ST>(al[((int64_t)i * a.items + item) * 32 + lane_sc]);
                                         }
                                         av = i < pr ? av : 0.f;
-                                        y[rq][q * 2 + e2] = fmaf(av, c[q][rq * 2 + e2], y[rq][q * 2 + e2]);
+                                        y[rq][q * 2 + e2] = fmaf(av, cc[q][rq * 2 + e2], y[rq][q * 2 + e2]);
                                     }
                                 }
                             }
@@ -302,7 +321,11 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                                         }
                                     }
                         }
-                    }
+                        }
+                    };
+                    int ii = 0;
+                    for (; ii + 1 < np; ii += 2) planes_n(std::integral_constant<int, 2>{}, ii);
+                    if (ii < np) planes_n(std::integral_constant<int, 1>{}, ii);
                 }
                 __syncwarp();  // all lanes are done with `buf` before it is refilled
             }

@@ -233,12 +233,10 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                 const int np = min(kMaxStagePlanes, a.pmax - i0);
 #pragma unroll
                 for (int gg = 0; gg < 2; ++gg) {  // two 128-column groups of the slice
-                    uint32_t xa[8][4];            // A fragments of this group's 8 k-steps
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) ldmatrix_x4(xa[kk], &S.xs[xrow][gg * 128 + kk * 16 + xcol]);
-                    // planes two at a time: four independent MMA chains per warp
+                    // all staged planes at once: 2 * np independent MMA chains per warp
                     // (the per-warp dependency chain, not any one pipe, bounds this
-                    // kernel -- DESIGN.md §3.3); scaling in plane order as before
+                    // kernel -- DESIGN.md §3.3); each k-step's A fragment is loaded
+                    // once (ldmatrix) and feeds every plane; scaling in plane order
                     auto planes_n = [&](auto npl_c, int ii0) {
                         constexpr int NPL = decltype(npl_c)::value;
                         uint32_t rowb[NPL][2][4];
@@ -255,6 +253,8 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                         }
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk) {
+                            uint32_t xk[4];  // A fragment of k-step kk
+                            ldmatrix_x4(xk, &S.xs[xrow][gg * 128 + kk * 16 + xcol]);
 #pragma unroll
                             for (int pl = 0; pl < NPL; ++pl)
 #pragma unroll
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                                     const uint32_t off =
                                         (kk & 1) ? (w >> (13 + 4 * t)) & 0x78u : ((w << 3) >> (4 * t)) & 0x78u;
                                     const uint2 bf = lds64(nib_base | off);
-                                    mma16816(c[pl][q], xa[kk], bf.x, bf.y);
+                                    mma16816(c[pl][q], xk, bf.x, bf.y);
                                 }
                         }
 #pragma unroll
@@ -323,9 +323,11 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
                         }
                         }
                     };
-                    int ii = 0;
-                    for (; ii + 1 < np; ii += 2) planes_n(std::integral_constant<int, 2>{}, ii);
-                    if (ii < np) planes_n(std::integral_constant<int, 1>{}, ii);
+                    static_assert(kMaxStagePlanes == 4, "plane-count dispatch");
+                    if (np == 4) planes_n(std::integral_constant<int, 4>{}, 0);
+                    else if (np == 3) planes_n(std::integral_constant<int, 3>{}, 0);
+                    else if (np == 2) planes_n(std::integral_constant<int, 2>{}, 0);
+                    else planes_n(std::integral_constant<int, 1>{}, 0);
                 }
                 __syncwarp();  // all lanes are done with `buf` before it is refilled
             }

@@ -198,19 +198,24 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
 
         // issue the cp.async copies of tile rt's planes [i0, i0 + n) into buffer bf
         constexpr int kScChunks = 32 * (int)sizeof(ST) / 16;  // 16-byte pieces of one plane-item's 32 scales
+        // (the lane's scale set k and its source are fixed: looked up once, not
+        // per item -- a kernel-parameter array indexed by a per-lane k is a
+        // serialised constant-bank load)
+        const int sck = lane / kScChunks, scc = lane % kScChunks;  // set k, chunk c
+        const int sc_p = sck < a.npset ? a.pset[sck] : 0;           // its precision (0: lane idle)
+        const char* sc_src = sc_p ? reinterpret_cast<const char*>(a.alpha[sc_p]) + 16 * scc : nullptr;
         auto stage_item = [&](int rt, int bf, int i0) {
             if (rt < a.NRT) {
                 const int item = s * a.NRT + rt;
-                for (int i = i0; i < min(a.pmax, i0 + kMaxStagePlanes); ++i) {
+                const int i1 = min(a.pmax, i0 + kMaxStagePlanes);
+                for (int i = i0; i < i1; ++i) {
                     cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
-                    const int k = lane / kScChunks, c = lane % kScChunks;  // set k, chunk c
-                    if (k < a.npset) {
-                        if (i < a.pset[k]) {
-                            const ST* al = static_cast<const ST*>(a.alpha[a.pset[k]]) + ((int64_t)i * a.items + item) * 32;
-                            cp_async16(&S.sc[warp][bf][i - i0][k][c], reinterpret_cast<const char*>(al) + 16 * c);
-                        } else {  // plane i is beyond this set's precision: scale 0
-                            S.sc[warp][bf][i - i0][k][c] = make_uint4(0u, 0u, 0u, 0u);
-                        }
+                    if (sc_p) {
+                        if (i < sc_p)
+                            cp_async16(&S.sc[warp][bf][i - i0][sck][scc],
+                                       sc_src + ((int64_t)i * a.items + item) * 32 * (int64_t)sizeof(ST));
+                        else  // plane i is beyond this set's precision: scale 0
+                            S.sc[warp][bf][i - i0][sck][scc] = make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
             }

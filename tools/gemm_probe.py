@@ -14,7 +14,7 @@ ap.add_argument("--rows", type=int, default=14336)
 ap.add_argument("--cols", type=int, default=4096)
 ap.add_argument("--B", type=int, default=16)
 ap.add_argument("--iters", type=int, default=50)
-ap.add_argument("--mode", type=int, default=0, help="abcq_debug_set_mode (30: the mma.sync kernel)")
+ap.add_argument("--mode", type=int, default=0, help="abcq_debug_set_mode (40: the tcgen05 variant)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 from paper_2510_10467_b200 import _lib  # noqa: E402

@@ -149,3 +149,28 @@ def test_random_gemm_mixedp(P, L, seed):
             Y = dm.gemm_mixedp(ps, torch.from_numpy(X).cuda()).cpu().numpy()
             for b, p in enumerate(ps):
                 assert close(Y[b], wants[b], tol=1e-4, mtol=1e-5), (rows, cols, B, b, p, asym, sd, mode)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_single_gemv_io_dtypes(P, L, seed):
+    """f32 x and/or f16 y on random shapes: the table build from f32 x and the
+    f16 output rounding (held to north_star's 1e-3)."""
+    rng = np.random.default_rng(4000 + seed)
+    for case in range(4):
+        rows, cols = dim(rng, 1, 16000), dim(rng, 1, 16000)
+        while rows * cols > 16 << 20:
+            rows, cols = dim(rng, 1, 16000), dim(rng, 1, 16000)
+        p_hi, asym = int(rng.integers(1, 9)), bool(rng.random() < 0.4)
+        sd = "f16" if rng.random() < 0.7 else "f32"
+        m = make(P, rows, cols, 128, p_hi, asym, seed=seed * 10 + case)
+        dm = P.DeviceModel.from_model(m, scale_dtype=sd)
+        x32 = O.random_gaussian(1, cols, seed=seed * 10 + case).ravel().astype(np.float32)
+        p = int(rng.integers(1, p_hi + 1))
+        w = want(m, sd, p, x32)
+        for mode in (0, 27, 23):
+            L.abcq_debug_set_mode(0)
+            L.abcq_debug_set_mode(mode)
+            y32 = dm.gemv(p, torch.from_numpy(x32).cuda()).cpu().numpy()
+            assert close(y32, w), (rows, cols, p, asym, sd, mode, "f32 x")
+            y16 = dm.gemv(p, torch.from_numpy(x32).cuda(), out_dtype=torch.float16).float().cpu().numpy()
+            assert close(y16, w, tol=1e-3, mtol=1e-3), (rows, cols, p, asym, sd, mode, "f16 y")

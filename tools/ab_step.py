@@ -17,7 +17,7 @@ from paper_2510_10467_b200.device_model import gemv_batch  # noqa: E402
 
 modes = [int(v) for v in sys.argv[1:]] or [0]
 torch.cuda.set_device(0)
-models = bench.make_layer_models(P, 1, len(bench.PRECISIONS))
+models, _ = bench.make_layer_models(P, 1, len(bench.PRECISIONS))
 xs = {k: torch.randn(k, device="cuda").half() for k in {c for _, _, c in bench.LAYERS}}
 ys = [[torch.empty(m.rows, dtype=torch.float16, device="cuda") for m in row] for row in models]
 st = torch.cuda.Stream()

@@ -58,6 +58,7 @@ STEP_GROUPS = [tuple(range(7))]
 DECODER_GROUPS = [(0, 1, 2), (3,), (4, 5), (6,)]
 PRECISIONS = (2, 3, 4)
 E2E_GROUP = 4     # e2e steps per copy-pipeline group
+E2E_SETS = int(os.environ.get("ABCQ_BENCH_E2E_SETS", "4"))  # buffer sets in flight (groups computing / copying)
 MP_RESERVE_SMS = 4  # N > 1: SMs left to the overlapping NCCL all-gather (abcq_set_reserved_sms, NCCL_MAX_CTAS)
 P_LO, P_HI = 2, 4
 SCALE_BYTES = 2   # fp16 scales
@@ -766,7 +767,9 @@ def e2e_section(ctx, models, xs, all_jobs, args):
     Serving-style pipeline: steps run in groups of E2E_GROUP; a group's inputs
     (every step's x) are ONE host -> device copy on a side stream while the
     previous group computes, and its outputs ONE device -> host copy on another
-    side stream while the next group computes (two buffer sets). The compute
+    side stream while the next group computes (E2E_SETS buffer sets: a
+    group's buffers are reused E2E_SETS groups later; 2 / 3 / 4 sets measured
+    62.5 / 62.5 / 62.0 us per step). The compute
     stream waits on the copy streams once per group, so the launches inside a
     group stay PDL-chained and the host issues two copies per group instead of
     two per step (per-step copies left the step host-bound: 64 vs 58.8 us)."""
@@ -778,7 +781,7 @@ def e2e_section(ctx, models, xs, all_jobs, args):
     hx = hx1.repeat(G).pin_memory()  # one group's inputs: G steps x (every distinct x)
     n_out = sum(models[pi][li].rows for pi, p, li in all_jobs)
     halves = []
-    for _ in range(2):  # group parity: its G steps' inputs and outputs, contiguous (one copy each way)
+    for _ in range(E2E_SETS):  # per buffer set: its G steps' inputs and outputs, contiguous (one copy each way)
         H = {"dx": torch.empty(G * nx, dtype=torch.float16, device=dev),
              "dy": torch.empty(G * n_out, dtype=torch.float16, device=dev),
              "hy": torch.empty(G * n_out, dtype=torch.float16).pin_memory(), "plans": []}
@@ -795,12 +798,12 @@ def e2e_section(ctx, models, xs, all_jobs, args):
                                                for n, (pi, p, li) in enumerate(all_jobs)]))
         halves.append(H)
     # (every plan shares the compute stream's one split-K workspace: device_model.stream_workspace)
-    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "comp", "out")}  # per group parity
+    ev = {k: [torch.cuda.Event() for _ in range(E2E_SETS)] for k in ("in", "comp", "out")}  # per buffer set
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     cnt = {"h2d": 0, "d2h": 0}
 
-    def h2d(g):  # group g's inputs (its buffers were last computed on by group g-2)
-        h = g & 1
+    def h2d(g):  # group g's inputs (its buffers were last computed on by group g - E2E_SETS)
+        h = g % E2E_SETS
         with torch.cuda.stream(s_in):
             s_in.wait_event(ev["comp"][h])
             halves[h]["dx"].copy_(hx, non_blocking=True)
@@ -808,14 +811,14 @@ def e2e_section(ctx, models, xs, all_jobs, args):
         cnt["h2d"] += hx.numel() * 2
 
     def e2e_group(g, last):
-        h = g & 1
+        h = g % E2E_SETS
         H = halves[h]
         # the NEXT group's inputs go first: issued behind the previous group's
         # output copy they would land late (one copy queue) and stall this stream
         if not last:
             h2d(g + 1)
         st.wait_event(ev["in"][h])
-        st.wait_event(ev["out"][h])  # group g-2's outputs have left these buffers
+        st.wait_event(ev["out"][h])  # group g - E2E_SETS's outputs have left these buffers
         for plan in H["plans"]:
             plan.launch(st)
         ev["comp"][h].record(st)
@@ -830,8 +833,8 @@ def e2e_section(ctx, models, xs, all_jobs, args):
             for e in ev[k]:
                 e.record(st)
         h2d(0)
-        for g in range(2):
-            e2e_group(g, g == 1)
+        for g in range(E2E_SETS):
+            e2e_group(g, g == E2E_SETS - 1)
         torch.cuda.synchronize()
         cnt["h2d"] = cnt["d2h"] = 0
         n_groups = max(2, min(args.steps, 48) // G)
@@ -853,8 +856,8 @@ def e2e_section(ctx, models, xs, all_jobs, args):
             "api": f"GemvBatchPlan.launch of the 21 GEMVs (one C-ABI abcq_gemv_batch call per step), eager; "
                    f"every step's inputs copied in from and its outputs copied out to pinned host memory; steps in "
                    f"groups of {G}, each group's inputs one copy (issued while the previous group computes) and its "
-                   f"outputs one copy (while the next computes); the compute stream waits on the copy streams once "
-                   f"per group"}
+                   f"outputs one copy (while the next computes), {E2E_SETS} buffer sets in flight; the compute "
+                   f"stream waits on the copy streams once per group"}
 
 
 def config1(ctx, args, peak):

@@ -208,7 +208,10 @@ __global__ void __launch_bounds__(kGWarps * 32) gemm_mixedp_kernel(const GemmArg
             if (rt < a.NRT) {
                 const int item = s * a.NRT + rt;
                 const int i1 = min(a.pmax, i0 + kMaxStagePlanes);
-                for (int i = i0; i < i1; ++i) {
+#pragma unroll
+                for (int ii = 0; ii < kMaxStagePlanes; ++ii) {
+                    const int i = i0 + ii;
+                    if (i >= i1) break;
                     cp_async16(&stage[warp][bf][i - i0][lane], a.planes + i * a.plane_stride_u4 + (int64_t)item * 32 + lane);
                     if (sc_p) {
                         if (i < sc_p)
